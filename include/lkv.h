@@ -1,0 +1,324 @@
+/*
+ * lkv.h — C ABI of the B200-native LayerKV data-movement path.
+ *
+ * The reference (arXiv 2410.00428 artifact, "layersim") has no C ABI: its
+ * boundary is the C++ API of the static library layersim_core. This header is
+ * the thin, FFI-bindable layer under the C++ drop-in (include/layersim/ headers):
+ * plain structs, pointers and sizes, no C++ or torch types. Every entry point
+ * names the reference interface it replaces (paths relative to
+ * /root/reference/proj). INTEGRATION.md shows the ctypes binding a
+ * maintainer would add and where engine.cpp calls into the device half.
+ *
+ * Error convention (reference errors.hpp:9-17 + kv_manager.hpp:94-150):
+ *   capacity failures are VALUES (ok flags / has_value = 0), exactly where the
+ *   reference returns false / std::nullopt; logic errors are negative status
+ *   codes where the reference throws, with the exception text available from
+ *   lkv_last_error() (thread-local).
+ */
+#ifndef LKV_H_
+#define LKV_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define LKV_API __attribute__((visibility("default")))
+#else
+#define LKV_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------ */
+#define LKV_OK 0
+#define LKV_ERR_SIMULATION (-1) /* layersim::SimulationError */
+#define LKV_ERR_CONFIG (-2)     /* layersim::ConfigError */
+#define LKV_ERR_DOMAIN (-3)     /* std::domain_error */
+#define LKV_ERR_INVALID (-4)    /* std::invalid_argument / bad C argument */
+#define LKV_ERR_CUDA (-5)       /* CUDA runtime failure on the device path */
+#define LKV_ERR_CAPACITY (-6)   /* a device/host arena is too small */
+#define LKV_ERR_INTERNAL (-7)
+
+LKV_API const char* lkv_last_error(void);
+/* Build identification: "lkv <version> sm_100a" (also proves the .so loaded). */
+LKV_API const char* lkv_version(void);
+
+/* ---- value types (reference cost_model.hpp:9-43, kv_manager.hpp:13-78) --- */
+typedef struct lkv_model_spec {
+  int32_t n_layers, n_heads, n_kv_heads, d_head;
+  int64_t hidden;
+  double n_param;
+  int32_t f_precision;
+  int32_t pad_;
+} lkv_model_spec;
+
+typedef struct lkv_hardware_spec {
+  double flops, hbm_bandwidth, pcie_bandwidth;
+  int32_t nvlink, n_gpus;
+  double gpu_mem, kv_reserve_fraction;
+} lkv_hardware_spec;
+
+typedef struct lkv_cost_params {
+  double alpha, beta, gamma, delta;
+} lkv_cost_params;
+
+typedef struct lkv_pool_sizing {
+  int64_t max_input_tokens;
+  int32_t tokens_per_block;
+  int32_t pad_;
+  double activation_layers_factor, cpu_pool_multiple;
+} lkv_pool_sizing;
+
+typedef struct lkv_block_pools {
+  int64_t gpu_blocks_total, cpu_blocks_total;
+  int32_t tokens_per_block;
+  int32_t pad_;
+} lkv_block_pools;
+
+typedef struct lkv_offload_job {
+  int64_t job_id, request_id;
+  double bytes;
+  int32_t layer_count;
+  int32_t pad_;
+  int64_t gpu_blocks;
+} lkv_offload_job;
+
+typedef struct lkv_fetch_job {
+  int32_t layer;
+  int32_t pad_;
+  double bytes;
+} lkv_fetch_job;
+
+typedef struct lkv_freed_counts {
+  int64_t gpu, cpu, deferred_gpu;
+} lkv_freed_counts;
+
+#define LKV_LOC_NONE 0
+#define LKV_LOC_GPU 1
+#define LKV_LOC_CPU 2
+typedef struct lkv_slot_loc { /* reference kv_manager.hpp:44-49 */
+  uint8_t loc;
+  uint8_t offload_in_flight;
+  uint16_t pad_;
+  uint32_t slot;
+  uint32_t dest_slot;
+} lkv_slot_loc;
+
+#define LKV_OFFLOAD_HALF 0
+#define LKV_OFFLOAD_FULL 1
+
+/* ---- cost model (reference cost_model.hpp:48-78) ------------------------ */
+LKV_API int lkv_model_validate(const lkv_model_spec* m);
+LKV_API int lkv_kv_bytes_per_token_layer(const lkv_model_spec* m, int64_t* out);
+LKV_API int lkv_prefill_time(const lkv_model_spec*, const lkv_hardware_spec*, const lkv_cost_params*,
+                     int64_t seqlen, double* out);
+LKV_API int lkv_offload_time(const lkv_model_spec*, const lkv_hardware_spec*, const lkv_cost_params*,
+                     int64_t seqlen, int32_t layers_offloaded, double* out);
+LKV_API int lkv_min_retained_layers(const lkv_model_spec*, const lkv_hardware_spec*,
+                            const lkv_cost_params*, int64_t seqlen, int32_t* out);
+LKV_API int lkv_decode_step_time(const lkv_model_spec*, const lkv_hardware_spec*, const lkv_cost_params*,
+                         int64_t batch_kv_tokens, double* out);
+LKV_API int lkv_allreduce_time(const lkv_model_spec*, const lkv_hardware_spec*, int64_t tokens,
+                       double* out);
+
+/* ---- pool sizing / placement (reference kv_manager.hpp:27-40) ---------- */
+LKV_API int lkv_pool_size_from_hardware(const lkv_model_spec*, const lkv_hardware_spec*,
+                                const lkv_pool_sizing*, lkv_block_pools* out);
+/* retained[x], offloaded[n_layers - x] */
+LKV_API int lkv_layer_placement(int32_t n_layers, int32_t x, int32_t* retained, int32_t* offloaded);
+
+/* ---- KvManager (reference kv_manager.hpp:80-150) ------------------------ */
+typedef struct lkv_kv_manager lkv_kv_manager;
+
+typedef struct lkv_kv_stats {
+  int64_t gpu_blocks_total, gpu_blocks_free, cpu_blocks_total, cpu_blocks_free;
+  int32_t tokens_per_block, n_layers;
+  int64_t pending_offloads, live_requests;
+} lkv_kv_stats;
+
+LKV_API int lkv_kv_create(const lkv_block_pools* pools, const lkv_model_spec* model, lkv_kv_manager** out);
+LKV_API int lkv_kv_destroy(lkv_kv_manager* kv);
+LKV_API int lkv_kv_stats_get(const lkv_kv_manager* kv, lkv_kv_stats* out);
+LKV_API int lkv_kv_blocks_per_layer(const lkv_kv_manager*, int64_t tokens, int64_t* out);
+LKV_API int lkv_kv_request_wise_gpu_blocks(const lkv_kv_manager*, int64_t prompt_tokens, int64_t* out);
+LKV_API int lkv_kv_allocate_prefill(lkv_kv_manager*, int64_t request_id, int64_t prompt_tokens, int32_t x,
+                            int32_t* ok);
+LKV_API int lkv_kv_has_request(const lkv_kv_manager*, int64_t request_id, int32_t* out);
+/* request(id): sizes first, then the table (entries block-major: [b * L + l]). */
+LKV_API int lkv_kv_request_shape(const lkv_kv_manager*, int64_t request_id, int64_t* cached_tokens,
+                         int64_t* n_blocks);
+LKV_API int lkv_kv_request_table(const lkv_kv_manager*, int64_t request_id, lkv_slot_loc* entries,
+                         int64_t* token_begin, uint8_t* layer_residency);
+LKV_API int lkv_kv_retained_layer_count(const lkv_kv_manager*, int64_t request_id, int32_t* out);
+LKV_API int lkv_kv_gpu_blocks_held(const lkv_kv_manager*, int64_t request_id, int64_t* out);
+LKV_API int lkv_kv_gpu_row_cost(const lkv_kv_manager*, int64_t request_id, int64_t* out);
+LKV_API int lkv_kv_cpu_row_cost(const lkv_kv_manager*, int64_t request_id, int64_t* out);
+LKV_API int lkv_kv_offload_reclaim(const lkv_kv_manager*, int64_t request_id, int32_t mode, int64_t* out);
+LKV_API int lkv_kv_plan_offload(lkv_kv_manager*, int64_t request_id, int32_t mode, lkv_offload_job* job,
+                        int32_t* has_value);
+LKV_API int lkv_kv_complete_offload(lkv_kv_manager*, int64_t job_id);
+/* Writes min(cap, count) jobs; *count = number of jobs (call with cap 0 to size). */
+LKV_API int lkv_kv_plan_decode_fetch(const lkv_kv_manager*, int64_t request_id, lkv_fetch_job* out,
+                             int32_t cap, int32_t* count);
+LKV_API int lkv_kv_needs_append(const lkv_kv_manager*, int64_t request_id, int32_t* out);
+LKV_API int lkv_kv_append_decode_block(lkv_kv_manager*, int64_t request_id, int32_t* ok);
+LKV_API int lkv_kv_note_token(lkv_kv_manager*, int64_t request_id);
+LKV_API int lkv_kv_release(lkv_kv_manager*, int64_t request_id, lkv_freed_counts* out);
+LKV_API int lkv_kv_check_conservation(const lkv_kv_manager*);
+/* dump_table text. *len = bytes needed (no NUL); written when cap > *len. */
+LKV_API int lkv_kv_dump_table(const lkv_kv_manager*, char* buf, size_t cap, size_t* len);
+/* FNV-1a-64 of the dump_table text (the parity hash of BASELINE.md §2). */
+LKV_API int lkv_kv_dump_hash(const lkv_kv_manager*, uint64_t* out);
+
+/* ---- PcieBus, parity-mode timing (reference interconnect.hpp:9-80) ------ */
+typedef struct lkv_pcie_bus lkv_pcie_bus;
+#define LKV_D2H 0
+#define LKV_H2D 1
+typedef struct lkv_transfer_schedule {
+  double start, completion;
+  int32_t chunks, deferrals;
+} lkv_transfer_schedule;
+typedef struct lkv_span {
+  double begin, end;
+  int32_t is_allreduce;
+  int32_t pad_;
+} lkv_span;
+
+LKV_API int lkv_bus_create(double delta, lkv_pcie_bus** out);
+LKV_API int lkv_bus_destroy(lkv_pcie_bus*);
+LKV_API int lkv_bus_register_allreduce(lkv_pcie_bus*, double start, double duration,
+                               const lkv_hardware_spec* hw);
+LKV_API int lkv_bus_submit_transfer(lkv_pcie_bus*, double bytes, int32_t direction, double submit_time,
+                            double chunk_bytes, const lkv_hardware_spec* hw,
+                            lkv_transfer_schedule* out);
+LKV_API int lkv_bus_state(const lkv_pcie_bus*, double t, double* busy_until, double* allreduce_busy_until,
+                  int32_t* allreduce_active_at_t);
+LKV_API int lkv_bus_enable_history(lkv_pcie_bus*, int32_t on);
+LKV_API int lkv_bus_chunk_history(const lkv_pcie_bus*, lkv_span* out, int32_t cap, int32_t* count);
+LKV_API int lkv_bus_allreduce_windows(const lkv_pcie_bus*, lkv_span* out, int32_t cap, int32_t* count);
+
+/* schedule_prefill_span (reference engine.hpp:59-71, engine.cpp:22-45). */
+LKV_API int lkv_schedule_prefill_span(const lkv_model_spec*, const lkv_hardware_spec*,
+                              const lkv_cost_params*, lkv_pcie_bus*, const int32_t* offloaded,
+                              int32_t n_offloaded, int64_t prompt_tokens, double start,
+                              double chunk_bytes, int32_t transfers_enabled, double* completion,
+                              lkv_transfer_schedule* jobs, int32_t cap, int32_t* n_jobs);
+
+/* ======================================================================== *
+ * Device half (sm_100a). Replaces what the reference only models:
+ *   per-layer prefill KV write + D2H job   engine.cpp:35-42 (schedule_prefill_span)
+ *   escalation gather + D2H                kv_manager.cpp:222-288, engine.cpp:343-352
+ *   decode H2D fetch per layer             kv_manager.cpp:290-304, engine.cpp:426-449
+ *   paged decode attention                 cost_model.cpp:73-79 (decode_step_time)
+ * ======================================================================== */
+typedef struct lkv_device lkv_device;
+
+typedef struct lkv_device_config {
+  int32_t device;         /* CUDA ordinal */
+  int32_t tp_rank;        /* KV-head shard r of tp_size: kv heads [r*Hkv/N, (r+1)*Hkv/N) */
+  int32_t tp_size;
+  int32_t pipeline_depth; /* decode layers whose prefetch may be in flight (>= 1) */
+  int64_t gpu_slots;      /* device pool frames; must exceed the highest GPU slot id used */
+  int64_t host_slots;     /* pinned host frames; must exceed the highest CPU slot id used */
+  int64_t arena_slots;    /* prefetch arena frames per pipeline stage */
+  int32_t max_requests;   /* device block-table rows */
+  int32_t max_blocks;     /* logical blocks per request row */
+  int32_t max_batch;      /* decode batch members */
+  int32_t staging_chunks; /* D2H staging ring segments */
+  int64_t chunk_bytes;    /* D2H staging segment size (reference TransferJob.chunk_bytes) */
+} lkv_device_config;
+
+typedef struct lkv_device_info {
+  int64_t slot_bytes;   /* bytes of one (block, layer) slot on this GPU: bs * kvB / TP */
+  int32_t kv_heads_local, q_heads_local, head_dim, tokens_per_block;
+  void* pool;           /* device pool base, slot s at pool + s * slot_bytes */
+  void* host_pool;      /* pinned host pool base, CPU slot c at host_pool + c * slot_bytes */
+  void* arena;          /* device prefetch arena base */
+  void* compute_stream; /* cudaStream_t: scatter, gather, table sync, attention */
+  void* d2h_stream;     /* cudaStream_t: offload copies */
+  void* h2d_stream;     /* cudaStream_t: prefetch copies */
+} lkv_device_info;
+
+LKV_API int lkv_device_create(const lkv_model_spec* model, int32_t tokens_per_block,
+                      const lkv_device_config* cfg, lkv_device** out);
+LKV_API int lkv_device_destroy(lkv_device* dev);
+LKV_API int lkv_device_get_info(const lkv_device* dev, lkv_device_info* out);
+/* Attach as the table observer: every KvManager mutation is mirrored into the
+ * device block table and escalation jobs start their gather + D2H at
+ * plan_offload (engine.cpp:345-350); complete_offload waits for the job's
+ * copy to drain before the GPU send buffers are reused (engine.cpp:98-100). */
+LKV_API int lkv_device_bind(lkv_device* dev, lkv_kv_manager* kv);
+LKV_API int lkv_device_synchronize(lkv_device* dev);
+
+/* Prefill layer `layer` of a request produced K and V, each
+ * [tokens][kv_heads_local][head_dim] bf16 on the device (row pitch
+ * kv_heads_local*head_dim elements). Retained layers are scattered into
+ * their GPU slots; offloaded layers are packed into staging and streamed to
+ * the pinned host frames of their CPU slots on the D2H stream — the
+ * per-layer D2H job of schedule_prefill_span (engine.cpp:35-42). The
+ * kernels are ordered after work already on `stream` (NULL = compute
+ * stream) via an event. */
+LKV_API int lkv_prefill_layer(lkv_device* dev, int64_t request_id, int32_t layer, const void* k,
+                      const void* v, int64_t tokens, void* stream);
+/* 1 when the D2H copies of an escalation job have drained. */
+LKV_API int lkv_device_job_done(lkv_device* dev, int64_t job_id, int32_t* done);
+/* 1 when every prefill-layer D2H issued so far for this request has drained. */
+LKV_API int lkv_device_prefill_offload_done(lkv_device* dev, int64_t request_id, int32_t* done);
+
+/* Decode iteration (engine.cpp:405-453): snapshot the batch, plan per-layer
+ * fetches (plan_decode_fetch, kv_manager.cpp:290-304) and start the H2D of the
+ * first pipeline_depth layers into the arena. */
+LKV_API int lkv_decode_begin(lkv_device* dev, const int64_t* request_ids, int32_t n);
+/* Paged attention of one layer for the batch: q is device
+ * [n][q_heads_local][head_dim] bf16, out the same shape in out_dtype (bf16
+ * for serving, fp32 for parity checks); kv_len of member m = its
+ * cached_tokens at decode_begin. Waits for the layer's fetch, runs on the
+ * compute stream, then issues the fetch of layer + pipeline_depth. `scale` =
+ * softmax scale. */
+#define LKV_DTYPE_BF16 0
+#define LKV_DTYPE_F32 1
+LKV_API int lkv_decode_layer(lkv_device* dev, int32_t layer, const void* q, void* out, float scale,
+                             int32_t out_dtype);
+LKV_API int lkv_decode_end(lkv_device* dev);
+
+typedef struct lkv_decode_stats {
+  int64_t h2d_bytes_physical;    /* whole slots copied */
+  int64_t h2d_bytes_algorithmic; /* token-exact, = sum of plan_decode_fetch bytes */
+  int64_t h2d_copies;            /* cudaMemcpy(2D)Async calls */
+  int64_t kv_bytes_read;         /* token-exact K+V bytes the attention consumed */
+  int64_t attn_launches;
+  double attn_ms;                /* summed CUDA-event time of the attention launches */
+  double h2d_ms;                 /* CUDA-event span of the prefetch copies */
+  double iteration_ms;           /* decode_begin -> decode_end on the device */
+} lkv_decode_stats;
+LKV_API int lkv_device_set_timing(lkv_device* dev, int32_t on);
+LKV_API int lkv_decode_last_stats(const lkv_device* dev, lkv_decode_stats* out);
+
+typedef struct lkv_offload_stats {
+  int64_t d2h_bytes_physical, d2h_bytes_algorithmic, d2h_copies, jobs;
+  int64_t scatter_bytes;  /* slot bytes written by the scatter kernel */
+  double d2h_ms, pack_ms, scatter_ms;
+} lkv_offload_stats;
+LKV_API int lkv_offload_last_stats(const lkv_device* dev, lkv_offload_stats* out, int32_t reset);
+
+/* ---- synthetic KV and verification (tests, bench, smoke) ---------------- */
+/* K/V value of (layer, token, global kv head, dim): bf16 of a splitmix64
+ * draw in [-1, 1), see oracle/kvgen.c for the CPU restatement. Writes
+ * [tokens][kv_heads_local][head_dim] K and V for tokens [token0, token0+tokens). */
+LKV_API int lkv_fill_kv(lkv_device* dev, void* k, void* v, int64_t tokens, int64_t token0, int32_t layer,
+                uint64_t seed, void* stream);
+/* Counts elements of the request's KV (every layer, tokens < n_tokens) that
+ * differ from the generator, wherever they live now: GPU slots, or pinned
+ * host frames read directly by the kernel. */
+LKV_API int lkv_verify_request(lkv_device* dev, int64_t request_id, int64_t n_tokens, uint64_t seed,
+                       int64_t* mismatches);
+/* Writes generator data for every entry of a request (GPU slots and host
+ * frames) without going through prefill — bench setup only. */
+LKV_API int lkv_fill_request(lkv_device* dev, int64_t request_id, int64_t n_tokens, uint64_t seed);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LKV_H_ */

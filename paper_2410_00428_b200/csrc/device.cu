@@ -1,0 +1,926 @@
+// Device half of the LayerKV path (include/lkv.h "Device half").
+//
+// One lkv_device per GPU (per KV-head shard). It owns
+//   * HBM: one buffer [pool frames | depth x arena frames] so that the decode
+//     kernel addresses resident slots and prefetched frames uniformly; the
+//     device block-table mirror; a decode snapshot; D2H staging segments;
+//   * pinned host: the CPU slot pool (frame c = CPU slot c), a metadata
+//     upload ring (journal, slot lists, descriptors);
+//   * three streams: compute (table sync, scatter, pack, gather, attention),
+//     d2h (offload copies), h2d (prefetch copies), ordered by events only.
+// It is the KvManager's observer, so the reference call sequence (engine.cpp)
+// drives the device path without new calls for escalation jobs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <deque>
+#include <sstream>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "kernels.cuh"
+#include "layersim/errors.hpp"
+#include "layersim/kv_manager.hpp"
+#include "lkv.h"
+#include "lkv_internal.hpp"
+
+using layersim::KvManager;
+using layersim::Loc;
+using layersim::OffloadEntry;
+using layersim::OffloadJob;
+using layersim::RequestKv;
+
+namespace lkv {
+
+#define LKV_CUDA(expr)                                                                   \
+  do {                                                                                   \
+    cudaError_t e_ = (expr);                                                             \
+    if (e_ != cudaSuccess) {                                                             \
+      throw CudaError(std::string(#expr) + ": " + cudaGetErrorString(e_) + " (" __FILE__ \
+                      ":" + std::to_string(__LINE__) + ")");                             \
+    }                                                                                    \
+  } while (0)
+
+static int sm_count_of(int dev) {
+  int n = 0;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
+}
+
+// Pinned ring for small host->device metadata. Regions are released once the
+// event recorded after their consumer has completed.
+class UploadRing {
+ public:
+  void init(std::size_t bytes) {
+    LKV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&buf_), bytes, cudaHostAllocMapped));
+    cap_ = bytes;
+  }
+  void destroy() {
+    for (auto& r : live_) cudaEventDestroy(r.ev);
+    live_.clear();
+    if (buf_) cudaFreeHost(buf_);
+    buf_ = nullptr;
+  }
+  // Reserve `bytes` (16 B aligned); blocks on older consumers if needed.
+  char* reserve(std::size_t bytes) {
+    bytes = (bytes + 15) & ~std::size_t(15);
+    if (bytes > cap_) throw CapacityError("upload ring: request larger than ring");
+    if (head_ + bytes > cap_) head_ = 0;
+    const std::size_t lo = head_, hi = head_ + bytes;
+    while (!live_.empty()) {
+      const Region& r = live_.front();
+      const bool overlap = r.lo < hi && lo < r.hi;
+      if (!overlap && live_.size() < 4096) break;
+      LKV_CUDA(cudaEventSynchronize(r.ev));
+      cudaEventDestroy(r.ev);
+      live_.pop_front();
+    }
+    pending_lo_ = lo;
+    pending_hi_ = hi;
+    head_ = hi;
+    return buf_ + lo;
+  }
+  // Mark the last reserved region in use by work already enqueued on `s`.
+  void commit(cudaStream_t s) {
+    cudaEvent_t ev;
+    LKV_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    LKV_CUDA(cudaEventRecord(ev, s));
+    live_.push_back({pending_lo_, pending_hi_, ev});
+  }
+
+ private:
+  struct Region {
+    std::size_t lo, hi;
+    cudaEvent_t ev;
+  };
+  char* buf_ = nullptr;
+  std::size_t cap_ = 0, head_ = 0, pending_lo_ = 0, pending_hi_ = 0;
+  std::deque<Region> live_;
+};
+
+}  // namespace lkv
+
+using namespace lkv;
+
+struct lkv_device final : layersim::KvObserver {
+  // ---- shape
+  layersim::ModelSpec model;
+  lkv_device_config cfg{};
+  int L = 0, Hl = 0, Hql = 0, G = 0, D = 0, bs = 0, head0 = 0, sms = 148;
+  long long sb = 0;  // slot bytes on this GPU
+  long long seg_slots = 0;
+
+  // ---- memory
+  char* dbuf = nullptr;        // pool | arena stages
+  char* host_pool = nullptr;   // pinned, CPU slot frames
+  int* d_table = nullptr;      // [max_requests][L][max_blocks]
+  int* d_snap = nullptr;       // [L][arena_slots]
+  SeqDesc* d_seqs = nullptr;   // [max_batch]
+  char* d_staging = nullptr;   // staging_chunks x seg bytes
+  unsigned* d_slotlist = nullptr;  // staging_chunks x seg_slots GPU slot ids
+  float* d_part_o = nullptr;
+  float* d_part_ml = nullptr;
+  unsigned long long* d_counter = nullptr;
+  UploadRing ring;
+  static constexpr int kMaxSplits = 64;
+
+  // ---- streams / events
+  cudaStream_t cs = nullptr, d2h = nullptr, h2d = nullptr;
+  std::vector<cudaEvent_t> seg_ready, seg_free;
+  std::vector<char> seg_used;
+  int seg_next = 0;
+  std::vector<cudaEvent_t> fetch_done, attn_done;
+  std::vector<char> attn_recorded;
+
+  // ---- table mirror
+  KvManager* kv = nullptr;
+  std::unordered_map<long long, int> row_of;
+  std::vector<int> free_rows;
+  std::vector<TableUpdate> journal;
+
+  // ---- offload bookkeeping
+  std::unordered_map<long long, cudaEvent_t> job_ev;      // escalation job -> last copy
+  std::unordered_map<long long, cudaEvent_t> prefill_ev;  // request -> last prefill D2H
+  lkv_offload_stats ostats{};
+  bool timing = false;
+  cudaEvent_t t_pack0 = nullptr, t_pack1 = nullptr;
+
+  // ---- decode iteration
+  struct Member {
+    long long id;
+    int row, kv_len, nblk, blk_off;
+  };
+  std::vector<Member> members;
+  int total_blocks = 0, max_nblk = 0;
+  bool in_iteration = false;
+  lkv_decode_stats dstats{};
+  std::vector<cudaEvent_t> t_attn0, t_attn1;
+  cudaEvent_t t_it0 = nullptr, t_it1 = nullptr, t_h2d0 = nullptr, t_h2d1 = nullptr;
+  bool h2d_started = false;
+
+  // ======================================================================
+  void check_layer(int l) const {
+    if (l < 0 || l >= L) throw std::invalid_argument("layer out of range");
+  }
+
+  static void ev_create(cudaEvent_t* e, bool timed = false) {
+    LKV_CUDA(cudaEventCreateWithFlags(e, timed ? cudaEventDefault : cudaEventDisableTiming));
+  }
+
+  void init(const lkv_model_spec* m, int tpb, const lkv_device_config* c) {
+    model = to_model(m);
+    model.validate();
+    cfg = *c;
+    if (cfg.tp_size < 1 || cfg.tp_rank < 0 || cfg.tp_rank >= cfg.tp_size ||
+        model.n_kv_heads % cfg.tp_size != 0)
+      throw std::invalid_argument("tp_size must divide n_kv_heads and 0 <= tp_rank < tp_size");
+    if (model.d_head != 128) throw std::invalid_argument("device path supports d_head = 128");
+    if (model.f_precision != 2) throw std::invalid_argument("device path stores bf16 KV (f = 2)");
+    if (tpb != 16 && tpb != 32 && tpb != 64)
+      throw std::invalid_argument("tokens_per_block must be 16, 32 or 64");
+    L = model.n_layers;
+    D = model.d_head;
+    bs = tpb;
+    Hl = model.n_kv_heads / cfg.tp_size;
+    G = model.n_heads / model.n_kv_heads;
+    if (G * model.n_kv_heads != model.n_heads || (G != 1 && G != 2 && G != 4 && G != 8))
+      throw std::invalid_argument("GQA group size must be 1, 2, 4 or 8");
+    Hql = Hl * G;
+    head0 = cfg.tp_rank * Hl;
+    sb = 2ll * Hl * bs * D * 2;
+    if (cfg.pipeline_depth < 1) cfg.pipeline_depth = 2;
+    if (cfg.max_requests < 1 || cfg.max_blocks < 1 || cfg.max_batch < 1 || cfg.gpu_slots < 0 ||
+        cfg.host_slots < 0 || cfg.arena_slots < 0)
+      throw std::invalid_argument("device config sizes must be positive");
+    if (cfg.staging_chunks < 2) cfg.staging_chunks = 4;
+    if (cfg.chunk_bytes <= 0) cfg.chunk_bytes = 16ll << 20;
+    seg_slots = std::max<long long>(1, cfg.chunk_bytes / sb);
+
+    LKV_CUDA(cudaSetDevice(cfg.device));
+    sms = sm_count_of(cfg.device);
+    const long long frames = cfg.gpu_slots + cfg.arena_slots * cfg.pipeline_depth;
+    if (frames > 0x7FFFFFFFll) throw CapacityError("pool + arena frames exceed int32 indexing");
+    LKV_CUDA(cudaMalloc(&dbuf, std::max<long long>(frames, 1) * sb));
+    if (cfg.host_slots > 0)
+      LKV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool), cfg.host_slots * sb,
+                             cudaHostAllocMapped | cudaHostAllocPortable));
+    const long long tbl = static_cast<long long>(cfg.max_requests) * L * cfg.max_blocks;
+    LKV_CUDA(cudaMalloc(&d_table, tbl * sizeof(int)));
+    LKV_CUDA(cudaMemset(d_table, 0, tbl * sizeof(int)));
+    LKV_CUDA(cudaMalloc(&d_snap, std::max<long long>(1, static_cast<long long>(L) * cfg.arena_slots) *
+                                     sizeof(int)));
+    LKV_CUDA(cudaMalloc(&d_seqs, cfg.max_batch * sizeof(SeqDesc)));
+    LKV_CUDA(cudaMalloc(&d_staging, cfg.staging_chunks * seg_slots * sb));
+    LKV_CUDA(cudaMalloc(&d_slotlist, cfg.staging_chunks * seg_slots * sizeof(unsigned)));
+    const long long parts = static_cast<long long>(cfg.max_batch) * Hql * kMaxSplits;
+    LKV_CUDA(cudaMalloc(&d_part_o, parts * D * sizeof(float)));
+    LKV_CUDA(cudaMalloc(&d_part_ml, parts * 2 * sizeof(float)));
+    LKV_CUDA(cudaMalloc(&d_counter, sizeof(unsigned long long)));
+    ring.init(64ull << 20);
+
+    LKV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
+    LKV_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
+    LKV_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    seg_ready.resize(cfg.staging_chunks);
+    seg_free.resize(cfg.staging_chunks);
+    seg_used.assign(cfg.staging_chunks, 0);
+    for (int i = 0; i < cfg.staging_chunks; ++i) {
+      ev_create(&seg_ready[i]);
+      ev_create(&seg_free[i]);
+    }
+    fetch_done.resize(cfg.pipeline_depth);
+    attn_done.resize(cfg.pipeline_depth);
+    attn_recorded.assign(cfg.pipeline_depth, 0);
+    for (int i = 0; i < cfg.pipeline_depth; ++i) {
+      ev_create(&fetch_done[i]);
+      ev_create(&attn_done[i]);
+    }
+    t_attn0.resize(L);
+    t_attn1.resize(L);
+    for (int i = 0; i < L; ++i) {
+      ev_create(&t_attn0[i], true);
+      ev_create(&t_attn1[i], true);
+    }
+    ev_create(&t_it0, true);
+    ev_create(&t_it1, true);
+    ev_create(&t_h2d0, true);
+    ev_create(&t_h2d1, true);
+    ev_create(&t_pack0, true);
+    ev_create(&t_pack1, true);
+    for (int r = cfg.max_requests - 1; r >= 0; --r) free_rows.push_back(r);
+  }
+
+  ~lkv_device() override {
+    if (kv) kv->set_observer(nullptr);
+    cudaSetDevice(cfg.device);
+    if (cs) cudaStreamSynchronize(cs);
+    if (d2h) cudaStreamSynchronize(d2h);
+    if (h2d) cudaStreamSynchronize(h2d);
+    auto kill = [](std::vector<cudaEvent_t>& v) {
+      for (auto e : v)
+        if (e) cudaEventDestroy(e);
+    };
+    kill(seg_ready);
+    kill(seg_free);
+    kill(fetch_done);
+    kill(attn_done);
+    kill(t_attn0);
+    kill(t_attn1);
+    for (auto e : {t_it0, t_it1, t_h2d0, t_h2d1, t_pack0, t_pack1})
+      if (e) cudaEventDestroy(e);
+    for (auto& kvp : job_ev) cudaEventDestroy(kvp.second);
+    for (auto& kvp : prefill_ev) cudaEventDestroy(kvp.second);
+    ring.destroy();
+    cudaFree(dbuf);
+    if (host_pool) cudaFreeHost(host_pool);
+    cudaFree(d_table);
+    cudaFree(d_snap);
+    cudaFree(d_seqs);
+    cudaFree(d_staging);
+    cudaFree(d_slotlist);
+    cudaFree(d_part_o);
+    cudaFree(d_part_ml);
+    cudaFree(d_counter);
+    for (auto s : {cs, d2h, h2d})
+      if (s) cudaStreamDestroy(s);
+  }
+
+  // ---------------------------------------------------------------- table
+  static int enc(const layersim::SlotLoc& e) {
+    if (e.loc == Loc::Gpu) return static_cast<int>(e.slot);
+    if (e.loc == Loc::Cpu) return ~static_cast<int>(e.slot);
+    return ~0x7FFFFFFF;
+  }
+  long long tindex(int row, int l, int b) const {
+    return (static_cast<long long>(row) * L + l) * cfg.max_blocks + b;
+  }
+  void check_slot(const layersim::SlotLoc& e) const {
+    if (e.loc == Loc::Gpu && static_cast<long long>(e.slot) >= cfg.gpu_slots)
+      throw CapacityError("GPU slot " + std::to_string(e.slot) + " >= device pool frames " +
+                          std::to_string(cfg.gpu_slots));
+    if (e.loc == Loc::Cpu && static_cast<long long>(e.slot) >= cfg.host_slots)
+      throw CapacityError("CPU slot " + std::to_string(e.slot) + " >= pinned host frames " +
+                          std::to_string(cfg.host_slots));
+  }
+
+  void flush() {
+    if (journal.empty()) return;
+    const std::size_t n = journal.size();
+    auto* dst = reinterpret_cast<TableUpdate*>(ring.reserve(n * sizeof(TableUpdate)));
+    std::memcpy(dst, journal.data(), n * sizeof(TableUpdate));
+    const int threads = 256;
+    const int grid = static_cast<int>(std::min<std::size_t>((n + threads - 1) / threads, 4 * sms));
+    table_apply_kernel<<<grid, threads, 0, cs>>>(dst, static_cast<int>(n), d_table);
+    LKV_CUDA(cudaGetLastError());
+    ring.commit(cs);
+    journal.clear();
+  }
+
+  int row_for(long long id) const {
+    auto it = row_of.find(id);
+    if (it == row_of.end()) throw layersim::SimulationError("device: request " + std::to_string(id) + " has no table row");
+    return it->second;
+  }
+
+  void on_allocate(std::int64_t id, const RequestKv& r) override {
+    if (free_rows.empty()) throw CapacityError("device: all block-table rows in use");
+    if (static_cast<long long>(r.blocks.size()) > cfg.max_blocks)
+      throw CapacityError("device: request exceeds max_blocks per table row");
+    const int row = free_rows.back();
+    free_rows.pop_back();
+    row_of[id] = row;
+    journal.reserve(journal.size() + r.blocks.size() * L);
+    for (std::size_t b = 0; b < r.blocks.size(); ++b)
+      for (int l = 0; l < L; ++l) {
+        const auto& e = r.blocks[b].layers[l];
+        check_slot(e);
+        journal.push_back({tindex(row, l, static_cast<int>(b)), enc(e), 0});
+      }
+  }
+
+  void on_append(std::int64_t id, const RequestKv& r) override {
+    const int row = row_for(id);
+    const int b = static_cast<int>(r.blocks.size()) - 1;
+    if (b >= cfg.max_blocks) throw CapacityError("device: request exceeds max_blocks per table row");
+    for (int l = 0; l < L; ++l) {
+      const auto& e = r.blocks[b].layers[l];
+      check_slot(e);
+      journal.push_back({tindex(row, l, b), enc(e), 0});
+    }
+  }
+
+  void on_release(std::int64_t id, const RequestKv&) override {
+    auto it = row_of.find(id);
+    if (it == row_of.end()) return;
+    free_rows.push_back(it->second);
+    row_of.erase(it);
+    // Freed CPU frames may be rewritten by a later D2H: order those copies
+    // after every prefetch already reading them.
+    cudaEvent_t ev;
+    ev_create(&ev);
+    LKV_CUDA(cudaEventRecord(ev, h2d));
+    LKV_CUDA(cudaStreamWaitEvent(d2h, ev, 0));
+    cudaEventDestroy(ev);
+    auto pe = prefill_ev.find(id);
+    if (pe != prefill_ev.end()) {
+      cudaEventDestroy(pe->second);
+      prefill_ev.erase(pe);
+    }
+  }
+
+  // ------------------------------------------------------- D2H staging pipeline
+  // Copy `n` frames between a contiguous side and an arbitrary frame list,
+  // coalescing runs of constant positive stride into one 2D copy each.
+  int emit_copies(char* dst_base, const long long* dst_frames, const char* src_base,
+                  const long long* src_frames, long long n, cudaMemcpyKind kind,
+                  cudaStream_t s) {
+    int copies = 0;
+    long long i = 0;
+    while (i < n) {
+      long long j = i + 1;
+      long long dd = 0, ds = 0;
+      if (j < n) {
+        dd = dst_frames[j] - dst_frames[i];
+        ds = src_frames[j] - src_frames[i];
+        if (dd > 0 && ds > 0) {
+          while (j + 1 < n && dst_frames[j + 1] - dst_frames[j] == dd &&
+                 src_frames[j + 1] - src_frames[j] == ds)
+            ++j;
+          ++j;
+        } else {
+          j = i + 1;
+        }
+      }
+      const long long len = j - i;
+      char* d = dst_base + dst_frames[i] * sb;
+      const char* sp = src_base + src_frames[i] * sb;
+      if (len == 1 || (dd == 1 && ds == 1)) {
+        LKV_CUDA(cudaMemcpyAsync(d, sp, len * sb, kind, s));
+      } else {
+        LKV_CUDA(cudaMemcpy2DAsync(d, dd * sb, sp, ds * sb, sb, len, kind, s));
+      }
+      ++copies;
+      i = j;
+    }
+    return copies;
+  }
+
+  int next_segment() {
+    const int i = seg_next;
+    seg_next = (seg_next + 1) % cfg.staging_chunks;
+    if (seg_used[i]) LKV_CUDA(cudaStreamWaitEvent(cs, seg_free[i], 0));
+    seg_used[i] = 1;
+    return i;
+  }
+
+  // Stream frames [i0, i0+n) of a staging producer to host frames cpu[...].
+  void d2h_segment(int seg, const long long* cpu_frames, long long n) {
+    LKV_CUDA(cudaEventRecord(seg_ready[seg], cs));
+    LKV_CUDA(cudaStreamWaitEvent(d2h, seg_ready[seg], 0));
+    std::vector<long long> src(n);
+    for (long long i = 0; i < n; ++i) src[i] = seg * seg_slots + i;
+    ostats.d2h_copies +=
+        emit_copies(host_pool, cpu_frames, d_staging, src.data(), n, cudaMemcpyDeviceToHost, d2h);
+    ostats.d2h_bytes_physical += n * sb;
+    LKV_CUDA(cudaEventRecord(seg_free[seg], d2h));
+  }
+
+  void on_offload_planned(const OffloadJob& job, const std::vector<OffloadEntry>& entries) override {
+    flush();
+    const long long n = static_cast<long long>(entries.size());
+    long long tokens = 0;
+    for (const auto& e : entries) {
+      if (static_cast<long long>(e.cpu_slot) >= cfg.host_slots)
+        throw CapacityError("CPU slot " + std::to_string(e.cpu_slot) + " >= pinned host frames");
+      tokens += e.filled_tokens;
+    }
+    for (long long i0 = 0; i0 < n; i0 += seg_slots) {
+      const long long cnt = std::min(seg_slots, n - i0);
+      const int seg = next_segment();
+      auto* slots = reinterpret_cast<unsigned*>(ring.reserve(cnt * sizeof(unsigned)));
+      std::vector<long long> cpu(cnt);
+      for (long long i = 0; i < cnt; ++i) {
+        slots[i] = entries[i0 + i].gpu_slot;
+        cpu[i] = entries[i0 + i].cpu_slot;
+      }
+      unsigned* dl = d_slotlist + seg * seg_slots;
+      LKV_CUDA(cudaMemcpyAsync(dl, slots, cnt * sizeof(unsigned), cudaMemcpyHostToDevice, cs));
+      ring.commit(cs);
+      const int grid = static_cast<int>(std::min<long long>(4ll * sms, (cnt * sb / 16 + 255) / 256));
+      gather_slots_kernel<<<std::max(grid, 1), 256, 0, cs>>>(dbuf, dl, static_cast<int>(cnt), sb,
+                                                             d_staging + seg * seg_slots * sb);
+      LKV_CUDA(cudaGetLastError());
+      d2h_segment(seg, cpu.data(), cnt);
+    }
+    cudaEvent_t ev;
+    ev_create(&ev);
+    LKV_CUDA(cudaEventRecord(ev, d2h));
+    job_ev[job.job_id] = ev;
+    ostats.jobs += 1;
+    ostats.d2h_bytes_algorithmic += tokens * (sb / bs);
+  }
+
+  void on_offload_complete(std::int64_t job_id, std::int64_t rid, bool orphaned,
+                           const RequestKv*) override {
+    auto it = job_ev.find(job_id);
+    if (it != job_ev.end()) {
+      LKV_CUDA(cudaEventSynchronize(it->second));  // send buffers drained
+      cudaEventDestroy(it->second);
+      job_ev.erase(it);
+    }
+    if (orphaned) return;
+    const int row = row_for(rid);
+    for (const auto& e : kv->offload_entries(job_id))
+      journal.push_back({tindex(row, e.layer, e.block), ~static_cast<int>(e.cpu_slot), 0});
+  }
+
+  // ---------------------------------------------------------------- prefill
+  void prefill_layer(long long id, int l, const void* k, const void* v, long long tokens,
+                     cudaStream_t user) {
+    check_layer(l);
+    flush();
+    if (user && user != cs) {
+      cudaEvent_t ev;
+      ev_create(&ev);
+      LKV_CUDA(cudaEventRecord(ev, user));
+      LKV_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      cudaEventDestroy(ev);
+    }
+    const RequestKv& r = kv->request(id);
+    const int row = row_for(id);
+    const long long nb = std::min<long long>((tokens + bs - 1) / bs, static_cast<long long>(r.blocks.size()));
+    if (tokens > static_cast<long long>(r.blocks.size()) * bs)
+      throw std::invalid_argument("prefill_layer: more tokens than allocated blocks");
+    if (timing) LKV_CUDA(cudaEventRecord(t_pack0, cs));
+    // GPU-resident blocks: scatter through the table mirror (CPU entries skipped).
+    long long n_gpu = 0;
+    for (long long b = 0; b < nb; ++b) n_gpu += r.blocks[b].layers[l].loc == Loc::Gpu;
+    const auto* kb = static_cast<const __nv_bfloat16*>(k);
+    const auto* vb = static_cast<const __nv_bfloat16*>(v);
+    if (n_gpu == nb && nb > 0) {
+      const long long vecs = nb * sb / 16;
+      const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
+      scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, 0, static_cast<int>(nb),
+                                              d_table + tindex(row, l, 0), dbuf, sb, Hl, bs, D);
+      LKV_CUDA(cudaGetLastError());
+      ostats.scatter_bytes += nb * sb;
+    } else {
+      // Runs of blocks by residency; GPU runs scatter, CPU runs pack+D2H.
+      long long b = 0;
+      while (b < nb) {
+        const Loc where = r.blocks[b].layers[l].loc;
+        long long e = b + 1;
+        while (e < nb && r.blocks[e].layers[l].loc == where) ++e;
+        if (where == Loc::Gpu) {
+          const long long vecs = (e - b) * sb / 16;
+          const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
+          scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b), static_cast<int>(e - b),
+                                                  d_table + tindex(row, l, 0), dbuf, sb, Hl, bs, D);
+          LKV_CUDA(cudaGetLastError());
+          ostats.scatter_bytes += (e - b) * sb;
+        } else if (where == Loc::Cpu) {
+          for (long long c0 = b; c0 < e; c0 += seg_slots) {
+            const long long cnt = std::min(seg_slots, e - c0);
+            const int seg = next_segment();
+            const long long vecs = cnt * sb / 16;
+            const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
+            scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(c0), static_cast<int>(cnt),
+                                                    nullptr, d_staging + seg * seg_slots * sb, sb, Hl, bs, D);
+            LKV_CUDA(cudaGetLastError());
+            std::vector<long long> cpu(cnt);
+            for (long long i = 0; i < cnt; ++i) {
+              const auto& en = r.blocks[c0 + i].layers[l];
+              check_slot(en);
+              cpu[i] = en.slot;
+            }
+            d2h_segment(seg, cpu.data(), cnt);
+            const long long tok_hi = std::min(tokens, (c0 + cnt) * bs);
+            ostats.d2h_bytes_algorithmic += (tok_hi - c0 * bs) * (sb / bs);
+          }
+        }
+        b = e;
+      }
+      cudaEvent_t& ev = prefill_ev[id];
+      if (!ev) ev_create(&ev);
+      LKV_CUDA(cudaEventRecord(ev, d2h));
+    }
+    if (timing) LKV_CUDA(cudaEventRecord(t_pack1, cs));
+  }
+
+  // ----------------------------------------------------------------- decode
+  void issue_fetch(int l) {
+    const int st = l % cfg.pipeline_depth;
+    if (attn_recorded[st]) LKV_CUDA(cudaStreamWaitEvent(h2d, attn_done[st], 0));
+    if (timing && !h2d_started) {
+      LKV_CUDA(cudaEventRecord(t_h2d0, h2d));
+      h2d_started = true;
+    }
+    const long long arena0 = cfg.gpu_slots + static_cast<long long>(st) * cfg.arena_slots;
+    std::vector<long long> src, dst;
+    for (const Member& m : members) {
+      const RequestKv& r = kv->request(m.id);
+      src.clear();
+      dst.clear();
+      long long tok = 0;
+      for (int b = 0; b < m.nblk; ++b) {
+        const auto& e = r.blocks[b].layers[l];
+        if (e.loc != Loc::Cpu) continue;
+        check_slot(e);
+        src.push_back(e.slot);
+        dst.push_back(arena0 + m.blk_off + b);
+        tok += std::clamp<long long>(m.kv_len - static_cast<long long>(b) * bs, 0, bs);
+      }
+      if (src.empty()) continue;
+      dstats.h2d_copies += emit_copies(dbuf, dst.data(), host_pool, src.data(),
+                                       static_cast<long long>(src.size()), cudaMemcpyHostToDevice, h2d);
+      dstats.h2d_bytes_physical += static_cast<long long>(src.size()) * sb;
+      dstats.h2d_bytes_algorithmic += tok * (sb / bs);
+    }
+    LKV_CUDA(cudaEventRecord(fetch_done[st], h2d));
+    if (timing) LKV_CUDA(cudaEventRecord(t_h2d1, h2d));
+  }
+
+  void decode_begin(const int64_t* ids, int n) {
+    if (in_iteration) throw layersim::SimulationError("decode_begin: iteration already open");
+    if (n < 0 || n > cfg.max_batch) throw CapacityError("decode batch exceeds max_batch");
+    flush();
+    members.clear();
+    total_blocks = 0;
+    max_nblk = 0;
+    dstats = lkv_decode_stats{};
+    h2d_started = false;
+    auto* desc = reinterpret_cast<SeqDesc*>(ring.reserve(std::max(n, 1) * sizeof(SeqDesc)));
+    for (int i = 0; i < n; ++i) {
+      const RequestKv& r = kv->request(ids[i]);
+      Member m;
+      m.id = ids[i];
+      m.row = row_for(ids[i]);
+      m.kv_len = static_cast<int>(r.cached_tokens);
+      m.nblk = static_cast<int>(std::min<long long>((r.cached_tokens + bs - 1) / bs, static_cast<long long>(r.blocks.size())));
+      m.blk_off = total_blocks;
+      total_blocks += m.nblk;
+      max_nblk = std::max(max_nblk, m.nblk);
+      members.push_back(m);
+      desc[i] = {static_cast<int>(tindex(m.row, 0, 0)), m.kv_len, m.blk_off, m.nblk};
+      dstats.kv_bytes_read += static_cast<long long>(m.kv_len) * (sb / bs) * L;
+    }
+    if (total_blocks > cfg.arena_slots)
+      throw CapacityError("decode batch needs " + std::to_string(total_blocks) +
+                          " arena frames per stage, have " + std::to_string(cfg.arena_slots));
+    if (timing) LKV_CUDA(cudaEventRecord(t_it0, cs));
+    LKV_CUDA(cudaMemcpyAsync(d_seqs, desc, std::max(n, 1) * sizeof(SeqDesc), cudaMemcpyHostToDevice, cs));
+    ring.commit(cs);
+    if (n > 0 && max_nblk > 0) {
+      // one launch resolves every layer; layer l's arena stage is l % depth
+      dim3 grid((max_nblk + 255) / 256, n, L);
+      decode_snapshot_kernel<<<grid, 256, 0, cs>>>(d_table, d_seqs, n, cfg.max_blocks, cfg.gpu_slots,
+                                                   cfg.arena_slots, cfg.pipeline_depth, d_snap);
+      LKV_CUDA(cudaGetLastError());
+    }
+    // Prefetches start after every D2H issued so far (the reference bus is
+    // serial: a layer's D2H precedes a later H2D of it).
+    cudaEvent_t ev;
+    ev_create(&ev);
+    LKV_CUDA(cudaEventRecord(ev, d2h));
+    LKV_CUDA(cudaStreamWaitEvent(h2d, ev, 0));
+    cudaEventDestroy(ev);
+    in_iteration = true;
+    for (int l = 0; l < std::min(cfg.pipeline_depth, L); ++l) issue_fetch(l);
+  }
+
+  template <int GG, int BB>
+  void launch_attn(int l, int n_split, int bps, const void* q, void* out, int f32, float scale_log2) {
+    dim3 grid(n_split, Hl, static_cast<unsigned>(members.size()));
+    decode_attn_kernel<GG, BB><<<grid, 128, 0, cs>>>(
+        dbuf, sb, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots, d_seqs,
+        static_cast<const __nv_bfloat16*>(q), out, f32, d_part_o,
+        d_part_ml, n_split, bps, scale_log2);
+  }
+
+  template <int GG>
+  void launch_attn_bs(int l, int n_split, int bps, const void* q, void* out, int f32, float sl2) {
+    if (bs == 16) launch_attn<GG, 16>(l, n_split, bps, q, out, f32, sl2);
+    else if (bs == 32) launch_attn<GG, 32>(l, n_split, bps, q, out, f32, sl2);
+    else launch_attn<GG, 64>(l, n_split, bps, q, out, f32, sl2);
+  }
+
+  void decode_layer(int l, const void* q, void* out, float scale, int f32) {
+    if (!in_iteration) throw layersim::SimulationError("decode_layer outside decode_begin/end");
+    check_layer(l);
+    const int st = l % cfg.pipeline_depth;
+    LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));
+    const int n = static_cast<int>(members.size());
+    if (timing) LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
+    if (n > 0) {
+      const int pairs = n * Hl;
+      const int target = 4 * sms;
+      int n_split = std::max(1, std::min((target + pairs - 1) / pairs, std::max(max_nblk, 1)));
+      int bps = (std::max(max_nblk, 1) + n_split - 1) / n_split;
+      bps = std::min(bps, 256);
+      n_split = (std::max(max_nblk, 1) + bps - 1) / bps;
+      if (n_split > kMaxSplits) {
+        n_split = kMaxSplits;
+        bps = (max_nblk + n_split - 1) / n_split;
+        if (bps > 256) throw CapacityError("decode: context too long for split table");
+      }
+      const float sl2 = scale * 1.4426950408889634f;
+      switch (G) {
+        case 1: launch_attn_bs<1>(l, n_split, bps, q, out, f32, sl2); break;
+        case 2: launch_attn_bs<2>(l, n_split, bps, q, out, f32, sl2); break;
+        case 4: launch_attn_bs<4>(l, n_split, bps, q, out, f32, sl2); break;
+        default: launch_attn_bs<8>(l, n_split, bps, q, out, f32, sl2); break;
+      }
+      LKV_CUDA(cudaGetLastError());
+      dstats.attn_launches += 1;
+      if (n_split > 1) {
+        decode_merge_kernel<<<n * Hql, D, 0, cs>>>(d_part_o, d_part_ml, n_split, D, out, f32);
+        LKV_CUDA(cudaGetLastError());
+      }
+    }
+    if (timing) LKV_CUDA(cudaEventRecord(t_attn1[l], cs));
+    LKV_CUDA(cudaEventRecord(attn_done[st], cs));
+    attn_recorded[st] = 1;
+    if (l + cfg.pipeline_depth < L) issue_fetch(l + cfg.pipeline_depth);
+  }
+
+  void decode_end() {
+    if (!in_iteration) throw layersim::SimulationError("decode_end without decode_begin");
+    in_iteration = false;
+    if (timing) {
+      LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[(L - 1) % cfg.pipeline_depth], 0));
+      LKV_CUDA(cudaEventRecord(t_it1, cs));
+    }
+  }
+};
+
+// ============================================================================
+#define LKV_TRY try {
+#define LKV_CATCH                               \
+  }                                             \
+  catch (...) {                                 \
+    return lkv::status_from_current_exception(); \
+  }                                             \
+  return LKV_OK;
+#define LKV_REQUIRE(cond)                         \
+  do {                                            \
+    if (!(cond)) {                                \
+      lkv::set_error("invalid argument: " #cond); \
+      return LKV_ERR_INVALID;                     \
+    }                                             \
+  } while (0)
+
+extern "C" {
+
+int lkv_device_create(const lkv_model_spec* m, int32_t tpb, const lkv_device_config* c,
+                      lkv_device** out) {
+  LKV_REQUIRE(m && c && out);
+  lkv_device* d = new lkv_device();
+  try {
+    d->init(m, tpb, c);
+  } catch (...) {
+    const int st = lkv::status_from_current_exception();
+    delete d;
+    return st;
+  }
+  *out = d;
+  return LKV_OK;
+}
+
+int lkv_device_destroy(lkv_device* d) {
+  delete d;
+  return LKV_OK;
+}
+
+int lkv_device_get_info(const lkv_device* d, lkv_device_info* o) {
+  LKV_REQUIRE(d && o);
+  o->slot_bytes = d->sb;
+  o->kv_heads_local = d->Hl;
+  o->q_heads_local = d->Hql;
+  o->head_dim = d->D;
+  o->tokens_per_block = d->bs;
+  o->pool = d->dbuf;
+  o->host_pool = d->host_pool;
+  o->arena = d->dbuf + d->cfg.gpu_slots * d->sb;
+  o->compute_stream = d->cs;
+  o->d2h_stream = d->d2h;
+  o->h2d_stream = d->h2d;
+  return LKV_OK;
+}
+
+int lkv_device_bind(lkv_device* d, lkv_kv_manager* kv) {
+  LKV_REQUIRE(d && kv);
+  LKV_TRY KvManager& k = lkv::kv_impl(kv);
+  if (k.n_layers() != d->L) throw std::invalid_argument("bind: layer count mismatch");
+  if (k.tokens_per_block() != d->bs) throw std::invalid_argument("bind: tokens_per_block mismatch");
+  if (!k.request_ids().empty()) throw std::invalid_argument("bind: manager already holds requests");
+  d->kv = &k;
+  k.set_observer(d);
+  LKV_CATCH
+}
+
+int lkv_device_synchronize(lkv_device* d) {
+  LKV_REQUIRE(d);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->flush();
+  LKV_CUDA(cudaStreamSynchronize(d->cs));
+  LKV_CUDA(cudaStreamSynchronize(d->d2h));
+  LKV_CUDA(cudaStreamSynchronize(d->h2d));
+  LKV_CATCH
+}
+
+int lkv_prefill_layer(lkv_device* d, int64_t id, int32_t layer, const void* k, const void* v,
+                      int64_t tokens, void* stream) {
+  LKV_REQUIRE(d && k && v && tokens >= 0 && d->kv);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->prefill_layer(id, layer, k, v, tokens, static_cast<cudaStream_t>(stream));
+  LKV_CATCH
+}
+
+int lkv_device_job_done(lkv_device* d, int64_t job_id, int32_t* done) {
+  LKV_REQUIRE(d && done);
+  LKV_TRY auto it = d->job_ev.find(job_id);
+  if (it == d->job_ev.end()) {
+    *done = 1;
+  } else {
+    const cudaError_t e = cudaEventQuery(it->second);
+    if (e != cudaSuccess && e != cudaErrorNotReady) LKV_CUDA(e);
+    *done = e == cudaSuccess ? 1 : 0;
+  }
+  LKV_CATCH
+}
+
+int lkv_device_prefill_offload_done(lkv_device* d, int64_t id, int32_t* done) {
+  LKV_REQUIRE(d && done);
+  LKV_TRY auto it = d->prefill_ev.find(id);
+  if (it == d->prefill_ev.end()) {
+    *done = 1;
+  } else {
+    const cudaError_t e = cudaEventQuery(it->second);
+    if (e != cudaSuccess && e != cudaErrorNotReady) LKV_CUDA(e);
+    *done = e == cudaSuccess ? 1 : 0;
+  }
+  LKV_CATCH
+}
+
+int lkv_decode_begin(lkv_device* d, const int64_t* ids, int32_t n) {
+  LKV_REQUIRE(d && d->kv && (ids || n == 0));
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->decode_begin(ids, n);
+  LKV_CATCH
+}
+
+int lkv_decode_layer(lkv_device* d, int32_t layer, const void* q, void* out, float scale,
+                     int32_t out_dtype) {
+  LKV_REQUIRE(d && q && out);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->decode_layer(layer, q, out, scale, out_dtype == LKV_DTYPE_F32 ? 1 : 0);
+  LKV_CATCH
+}
+
+int lkv_decode_end(lkv_device* d) {
+  LKV_REQUIRE(d);
+  LKV_TRY d->decode_end();
+  LKV_CATCH
+}
+
+int lkv_device_set_timing(lkv_device* d, int32_t on) {
+  LKV_REQUIRE(d);
+  d->timing = on != 0;
+  return LKV_OK;
+}
+
+int lkv_decode_last_stats(const lkv_device* dc, lkv_decode_stats* out) {
+  LKV_REQUIRE(dc && out);
+  lkv_device* d = const_cast<lkv_device*>(dc);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  *out = d->dstats;
+  if (d->timing && !d->in_iteration) {
+    LKV_CUDA(cudaEventSynchronize(d->t_it1));
+    float ms = 0.f;
+    double attn = 0.0;
+    for (int l = 0; l < d->L; ++l) {
+      if (cudaEventElapsedTime(&ms, d->t_attn0[l], d->t_attn1[l]) == cudaSuccess) attn += ms;
+    }
+    cudaGetLastError();
+    out->attn_ms = attn;
+    if (d->h2d_started && cudaEventElapsedTime(&ms, d->t_h2d0, d->t_h2d1) == cudaSuccess)
+      out->h2d_ms = ms;
+    cudaGetLastError();
+    if (cudaEventElapsedTime(&ms, d->t_it0, d->t_it1) == cudaSuccess) out->iteration_ms = ms;
+    cudaGetLastError();
+  }
+  LKV_CATCH
+}
+
+int lkv_offload_last_stats(const lkv_device* dc, lkv_offload_stats* out, int32_t reset) {
+  LKV_REQUIRE(dc && out);
+  lkv_device* d = const_cast<lkv_device*>(dc);
+  *out = d->ostats;
+  if (reset) d->ostats = lkv_offload_stats{};
+  return LKV_OK;
+}
+
+int lkv_fill_kv(lkv_device* d, void* k, void* v, int64_t tokens, int64_t token0, int32_t layer,
+                uint64_t seed, void* stream) {
+  LKV_REQUIRE(d && k && v && tokens >= 0 && token0 >= 0);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->cs;
+  const long long total = tokens * d->Hl * d->D;
+  if (total > 0) {
+    const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 8ll * d->sms));
+    fill_kv_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v),
+                                        tokens, token0, layer, d->Hl, d->head0, d->D, seed);
+    LKV_CUDA(cudaGetLastError());
+  }
+  LKV_CATCH
+}
+
+static void request_pass(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t seed, bool write,
+                         int64_t* mism) {
+  LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->flush();
+  const RequestKv& r = d->kv->request(id);
+  const int row = d->row_for(id);
+  const long long nb = std::min<long long>(static_cast<long long>(r.blocks.size()),
+                                           (n_tokens + d->bs - 1) / d->bs);
+  if (!write) LKV_CUDA(cudaMemsetAsync(d->d_counter, 0, sizeof(unsigned long long), d->cs));
+  // Host frames may still be landing from D2H copies.
+  LKV_CUDA(cudaStreamSynchronize(d->d2h));
+  if (nb > 0) {
+    dim3 grid(static_cast<unsigned>(nb), d->L);
+    if (write)
+      request_kv_kernel<true><<<grid, 256, 0, d->cs>>>(d->d_table + d->tindex(row, 0, 0), d->cfg.max_blocks,
+                                                       d->L, n_tokens, d->dbuf, d->host_pool, d->sb, d->Hl,
+                                                       d->head0, d->bs, d->D, seed, d->d_counter);
+    else
+      request_kv_kernel<false><<<grid, 256, 0, d->cs>>>(d->d_table + d->tindex(row, 0, 0), d->cfg.max_blocks,
+                                                        d->L, n_tokens, d->dbuf, d->host_pool, d->sb, d->Hl,
+                                                        d->head0, d->bs, d->D, seed, d->d_counter);
+    LKV_CUDA(cudaGetLastError());
+  }
+  if (!write) {
+    unsigned long long h = 0;
+    LKV_CUDA(cudaMemcpyAsync(&h, d->d_counter, sizeof h, cudaMemcpyDeviceToHost, d->cs));
+    LKV_CUDA(cudaStreamSynchronize(d->cs));
+    *mism = static_cast<int64_t>(h);
+  } else {
+    LKV_CUDA(cudaStreamSynchronize(d->cs));
+  }
+}
+
+int lkv_verify_request(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t seed,
+                       int64_t* mismatches) {
+  LKV_REQUIRE(d && d->kv && mismatches);
+  LKV_TRY request_pass(d, id, n_tokens, seed, false, mismatches);
+  LKV_CATCH
+}
+
+int lkv_fill_request(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t seed) {
+  LKV_REQUIRE(d && d->kv);
+  LKV_TRY request_pass(d, id, n_tokens, seed, true, nullptr);
+  LKV_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,433 @@
+// sm_100a kernels of the LayerKV data path. All of them are HBM-bound byte
+// movers or (decode attention) HBM-bound streaming reductions; none is
+// GEMM-shaped, so none uses tensor cores.
+//
+// Slot layout (one (block, layer) slot of one GPU's KV-head shard):
+//   [K | V][kv_heads_local][tokens_per_block][head_dim]  bf16
+// so one (slot, head) K or V tile is tokens_per_block * head_dim * 2 bytes
+// contiguous (4 KiB at bs=16, d=128).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kvgen.cuh"
+
+namespace lkv {
+
+struct uint4_ {
+  unsigned x, y, z, w;
+};
+
+__device__ __forceinline__ uint4 ld_stream(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+
+__device__ __forceinline__ void st_stream(void* p, const uint4& v) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1,%2,%3,%4};" ::"l"(p), "r"(v.x), "r"(v.y), "r"(v.z),
+               "r"(v.w)
+               : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// Block-table mirror: apply a journal of (index, value) updates. The journal
+// lives in pinned host memory and is read over the link directly (8-16 B per
+// update; a 32k-token allocation is 65 k updates).
+struct TableUpdate {
+  long long index;
+  int value;
+  int pad;
+};
+
+__global__ void table_apply_kernel(const TableUpdate* __restrict__ upd, int n,
+                                   int* __restrict__ table) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const TableUpdate u = upd[i];
+    table[u.index] = u.value;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Scatter / pack: contiguous prefill output K,V [tokens][Hl][D] -> slots.
+// Block b (tokens [b*bs, b*bs+bs)) goes to dst + frame[b] * slot_bytes, where
+// frame = the GPU slot ids from the table mirror (retained layer, scatter)
+// or b - b0 (offloaded layer, pack into a staging segment). Tokens past
+// `tokens` in the tail block are zero-filled. One 16 B vector per thread
+// step; consecutive threads write consecutive 16 B of a slot.
+__global__ void scatter_kv_kernel(const __nv_bfloat16* __restrict__ k,
+                                  const __nv_bfloat16* __restrict__ v, long long tokens,
+                                  int b0, int nblk, const int* __restrict__ frames,
+                                  char* __restrict__ dst, long long slot_bytes, int Hl, int bs,
+                                  int D) {
+  const int vec_per_row = D / 8;                        // 16 B vectors per (token, head)
+  const long long vec_per_slot = 2ll * Hl * bs * vec_per_row;
+  const long long total = vec_per_slot * nblk;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int bl = static_cast<int>(i / vec_per_slot);
+    long long r = i - bl * vec_per_slot;
+    const int c = static_cast<int>(r % vec_per_row);
+    r /= vec_per_row;
+    const int t = static_cast<int>(r % bs);
+    r /= bs;
+    const int h = static_cast<int>(r % Hl);
+    const int kvsel = static_cast<int>(r / Hl);
+    const int b = b0 + bl;
+    const long long tok = static_cast<long long>(b) * bs + t;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (tok < tokens) {
+      const __nv_bfloat16* src = (kvsel == 0 ? k : v) + (tok * Hl + h) * D + c * 8;
+      val = ld_stream(src);
+    }
+    const long long frame = frames ? frames[b] : bl;
+    char* out = dst + frame * slot_bytes +
+                ((static_cast<long long>(kvsel) * Hl + h) * bs + t) * (D * 2) + c * 16;
+    st_stream(out, val);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Gather: whole slots (list) -> contiguous staging, in list order.
+__global__ void gather_slots_kernel(const char* __restrict__ pool, const unsigned* __restrict__ slots,
+                                    int n, long long slot_bytes, char* __restrict__ dst) {
+  const long long vec_per_slot = slot_bytes / 16;
+  const long long total = vec_per_slot * n;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  // 4 independent 16 B loads in flight per thread per iteration.
+  for (; i + 3 * stride < total; i += 4 * stride) {
+    uint4 v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long j = i + u * stride;
+      const long long s = j / vec_per_slot;
+      v[u] = ld_stream(pool + static_cast<long long>(slots[s]) * slot_bytes +
+                       (j - s * vec_per_slot) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) st_stream(dst + (i + u * stride) * 16, v[u]);
+  }
+  for (; i < total; i += stride) {
+    const long long s = i / vec_per_slot;
+    st_stream(dst + i * 16,
+              ld_stream(pool + static_cast<long long>(slots[s]) * slot_bytes +
+                        (i - s * vec_per_slot) * 16));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Decode snapshot: resolve each (member, block) of one layer's table row into
+// a physical frame of the unified [pool | arena] buffer. GPU entries keep
+// their slot id; CPU entries (encoded ~cpu_slot) point at the arena frame the
+// prefetch writes: arena0 + member_base + b.
+struct SeqDesc {
+  int row_offset;   // table offset of (row, layer 0, block 0)
+  int kv_len;       // tokens attended
+  int blk_offset;   // this member's first entry in the snapshot / arena
+  int n_blocks;     // ceil(kv_len / bs)
+};
+
+__global__ void decode_snapshot_kernel(const int* __restrict__ table, const SeqDesc* __restrict__ seqs,
+                                       int n_seq, int max_blocks, long long pool_frames,
+                                       long long arena_frames, int depth, int* __restrict__ snap_all) {
+  const int m = blockIdx.y, layer = blockIdx.z;
+  if (m >= n_seq) return;
+  const SeqDesc sd = seqs[m];
+  const long long arena0 = pool_frames + (layer % depth) * arena_frames;
+  int* snap = snap_all + layer * arena_frames;
+  const int* row = table + sd.row_offset + static_cast<long long>(layer) * max_blocks;
+  for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < sd.n_blocks; b += gridDim.x * blockDim.x) {
+    const int e = row[b];
+    snap[sd.blk_offset + b] =
+        e >= 0 ? e : static_cast<int>(arena0 + sd.blk_offset + b);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Paged decode attention, split-K over blocks (flash-decoding style), GQA
+// group of G query heads per KV head handled by one CTA so each K/V byte is
+// read once. HBM-bound: per (seq, kv head) it streams kv_len*D*2*2 bytes.
+//
+// Work unit = a 16-token sub-tile of one block for one kv head: 4 KiB of K +
+// 4 KiB of V, loaded by one warp with 16 B vectors (lane: 16 B chunk c = dims
+// [8c, 8c+8) of rows r0 + 2k). Q.K partials are reduced across the 16 lanes
+// of a row pair with a value-splitting butterfly (8 shuffles for 8 rows).
+// Online softmax in the log2 domain; P.V accumulates fp32 per lane.
+template <int G, int BS>
+struct DecodeCfg {
+  static constexpr int kD = 128;
+  static constexpr int kWarps = 4;
+  static constexpr int kThreads = kWarps * 32;
+  static constexpr int kSubPerBlock = BS / 16;
+};
+
+// Attention output: bf16 (serving) or fp32 (parity checks at 1e-3 relative).
+__device__ __forceinline__ void store_out(void* out, int f32, long long i, float v) {
+  if (f32)
+    static_cast<float*>(out)[i] = v;
+  else
+    static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+}
+
+__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
+  const unsigned w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    f[2 * i] = __uint_as_float(w[i] << 16);
+    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+  }
+}
+
+template <int G, int BS>
+__global__ void __launch_bounds__(128) decode_attn_kernel(
+    const char* __restrict__ base, long long slot_bytes, int Hl,
+    const int* __restrict__ snap, const SeqDesc* __restrict__ seqs,
+    const __nv_bfloat16* __restrict__ q, void* __restrict__ out, int out_f32,
+    float* __restrict__ part_o, float* __restrict__ part_ml, int n_split, int blocks_per_split,
+    float scale_log2) {
+  using C = DecodeCfg<G, BS>;
+  constexpr int D = C::kD;
+  const int split = blockIdx.x, h = blockIdx.y, m = blockIdx.z;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = lane & 15, r0 = lane >> 4;
+  const int Hq = Hl * G;
+
+  __shared__ int s_tbl[256];
+  __shared__ float s_acc[C::kWarps][G][D];
+  __shared__ float s_m[C::kWarps][G], s_l[C::kWarps][G];
+
+  const SeqDesc sd = seqs[m];
+  const int jb0 = split * blocks_per_split;
+  const int jb1 = min(sd.n_blocks, jb0 + blocks_per_split);
+  const int nblk = max(0, jb1 - jb0);
+  for (int i = threadIdx.x; i < nblk; i += C::kThreads) s_tbl[i] = snap[sd.blk_offset + jb0 + i];
+
+  // q fragment: dims [8c, 8c+8) of each of the G heads, pre-scaled by
+  // softmax_scale * log2(e).
+  float qf[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    const uint4 u = *reinterpret_cast<const uint4*>(q + (static_cast<long long>(m) * Hq + h * G + g) * D + c * 8);
+    bf16x8_to_f32(u, qf[g]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) qf[g][i] *= scale_log2;
+  }
+  __syncthreads();
+
+  float mrun[G], lrun[G], acc[G][8];
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+    mrun[g] = -INFINITY;
+    lrun[g] = 0.f;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
+  }
+
+  const long long tile_bytes = static_cast<long long>(BS) * D * 2;  // one (slot, head) K tile
+  const int n_sub = nblk * C::kSubPerBlock;
+  for (int t = warp; t < n_sub; t += C::kWarps) {
+    const int jl = t / C::kSubPerBlock, sub = t % C::kSubPerBlock;
+    const int tok0 = (jb0 + jl) * BS + sub * 16;
+    const char* slot = base + static_cast<long long>(s_tbl[jl]) * slot_bytes;
+    const char* kp = slot + h * tile_bytes + sub * 16 * D * 2 + r0 * D * 2 + c * 16;
+    const char* vp = kp + static_cast<long long>(Hl) * tile_bytes;
+    uint4 kr[8], vr[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) kr[k] = ld_stream(kp + k * 2 * D * 2);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) vr[k] = ld_stream(vp + k * 2 * D * 2);
+
+    // ---- scores: s[g] for row = r0 + (c & 14)
+    float s[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float pr[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        float kf[8];
+        bf16x8_to_f32(kr[k], kf);
+        float a = 0.f;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a = fmaf(qf[g][i], kf[i], a);
+        pr[k] = a;
+      }
+      // butterfly over the 16 lanes sharing r0: 4 + 2 + 1 + 1 shuffles
+      const bool b3 = c & 8, b2 = c & 4, b1 = c & 2;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float send = b3 ? pr[j] : pr[j + 4];
+        const float keep = b3 ? pr[j + 4] : pr[j];
+        pr[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const float send = b2 ? pr[j] : pr[j + 2];
+        const float keep = b2 ? pr[j + 2] : pr[j];
+        pr[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+      }
+      {
+        const float send = b1 ? pr[0] : pr[1];
+        const float keep = b1 ? pr[1] : pr[0];
+        pr[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+      }
+      pr[0] += __shfl_xor_sync(0xffffffffu, pr[0], 1);
+      const int row = r0 + (c & 14);
+      s[g] = (tok0 + row < sd.kv_len) ? pr[0] : -INFINITY;
+    }
+
+    // ---- online softmax + P.V
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+      float mt = s[g];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
+      const float mnew = fmaxf(mrun[g], mt);
+      const float corr = (mrun[g] == -INFINITY) ? 0.f : exp2f(mrun[g] - mnew);
+      const float p = (s[g] == -INFINITY) ? 0.f : exp2f(s[g] - mnew);
+      lrun[g] = lrun[g] * corr + ((c & 1) ? 0.f : p);
+      mrun[g] = mnew;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[g][i] *= corr;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float pk = __shfl_sync(0xffffffffu, p, (lane & 16) + 2 * k);
+        float vf[8];
+        bf16x8_to_f32(vr[k], vf);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) acc[g][i] = fmaf(pk, vf[i], acc[g][i]);
+      }
+    }
+  }
+
+  // ---- warp reduce: rows split across r0 halves; l across all lanes
+#pragma unroll
+  for (int g = 0; g < G; ++g) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) acc[g][i] += __shfl_xor_sync(0xffffffffu, acc[g][i], 16);
+    float l = lrun[g];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (lane < 16) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s_acc[warp][g][c * 8 + i] = acc[g][i];
+    }
+    if (lane == 0) {
+      s_m[warp][g] = mrun[g];
+      s_l[warp][g] = l;
+    }
+  }
+  __syncthreads();
+
+  // ---- CTA merge of the warps, then final output or split partial
+  for (int idx = threadIdx.x; idx < G * D; idx += C::kThreads) {
+    const int g = idx / D, d = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < C::kWarps; ++w) M = fmaxf(M, s_m[w][g]);
+    float o = 0.f, L = 0.f;
+    if (M != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < C::kWarps; ++w) {
+        const float f = (s_m[w][g] == -INFINITY) ? 0.f : exp2f(s_m[w][g] - M);
+        o += f * s_acc[w][g][d];
+        L += f * s_l[w][g];
+      }
+    }
+    const long long hq = static_cast<long long>(m) * Hq + h * G + g;
+    if (n_split == 1) {
+      store_out(out, out_f32, hq * D + d, L > 0.f ? o / L : 0.f);
+    } else {
+      part_o[(hq * n_split + split) * D + d] = o;
+      if (d == 0) {
+        part_ml[(hq * n_split + split) * 2 + 0] = M;
+        part_ml[(hq * n_split + split) * 2 + 1] = L;
+      }
+    }
+  }
+}
+
+// Combine split partials: o = sum_s 2^(m_s - M) o_s / sum_s 2^(m_s - M) l_s.
+__global__ void decode_merge_kernel(const float* __restrict__ part_o,
+                                    const float* __restrict__ part_ml, int n_split, int D,
+                                    void* __restrict__ out, int out_f32) {
+  const long long hq = blockIdx.x;
+  const int d = threadIdx.x;
+  const float* ml = part_ml + hq * n_split * 2;
+  float M = -INFINITY;
+  for (int s = 0; s < n_split; ++s) M = fmaxf(M, ml[2 * s]);
+  float o = 0.f, L = 0.f;
+  if (M != -INFINITY) {
+    for (int s = 0; s < n_split; ++s) {
+      const float ms = ml[2 * s];
+      if (ms == -INFINITY) continue;
+      const float f = exp2f(ms - M);
+      o += f * part_o[(hq * n_split + s) * D + d];
+      L += f * ml[2 * s + 1];
+    }
+  }
+  if (d < D) store_out(out, out_f32, hq * D + d, L > 0.f ? o / L : 0.f);
+}
+
+// ---------------------------------------------------------------------------
+// Synthetic data and verification.
+__global__ void fill_kv_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v,
+                               long long tokens, long long token0, int layer, int Hl, int head0,
+                               int D, unsigned long long seed) {
+  const long long total = tokens * Hl * D;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = static_cast<int>(i % D);
+    const int h = static_cast<int>((i / D) % Hl);
+    const long long t = i / (static_cast<long long>(D) * Hl);
+    const unsigned short kb = kv_value_bf16(seed, layer, 0, token0 + t, head0 + h, d);
+    const unsigned short vb = kv_value_bf16(seed, layer, 1, token0 + t, head0 + h, d);
+    reinterpret_cast<unsigned short*>(k)[i] = kb;
+    reinterpret_cast<unsigned short*>(v)[i] = vb;
+  }
+}
+
+// One CTA per (block, layer) of a request: compare (or write) every element
+// of the slot against the generator. The slot is found through the table
+// mirror: GPU slot -> device pool, ~cpu_slot -> pinned host pool (read or
+// written directly over the link).
+template <bool kWrite>
+__global__ void request_kv_kernel(const int* __restrict__ table_row, int max_blocks, int n_layers,
+                                  long long n_tokens, char* __restrict__ pool,
+                                  char* __restrict__ host_pool, long long slot_bytes, int Hl,
+                                  int head0, int bs, int D, unsigned long long seed,
+                                  unsigned long long* __restrict__ mismatches) {
+  const int b = blockIdx.x, l = blockIdx.y;
+  const int e = table_row[static_cast<long long>(l) * max_blocks + b];
+  char* slot = e >= 0 ? pool + static_cast<long long>(e) * slot_bytes
+                      : host_pool + static_cast<long long>(~e) * slot_bytes;
+  unsigned short* s16 = reinterpret_cast<unsigned short*>(slot);
+  const int per_kv = Hl * bs * D;
+  unsigned long long bad = 0;
+  for (int i = threadIdx.x; i < 2 * per_kv; i += blockDim.x) {
+    const int kvsel = i / per_kv;
+    int r = i % per_kv;
+    const int d = r % D;
+    r /= D;
+    const int t = r % bs;
+    const int h = r / bs;
+    const long long tok = static_cast<long long>(b) * bs + t;
+    if (tok >= n_tokens) continue;
+    const unsigned short want = kv_value_bf16(seed, l, kvsel, tok, head0 + h, d);
+    if (kWrite)
+      s16[i] = want;
+    else
+      bad += (s16[i] != want);
+  }
+  if (!kWrite) {
+    for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
+    if ((threadIdx.x & 31) == 0 && bad) atomicAdd(mismatches, bad);
+  }
+}
+
+}  // namespace lkv

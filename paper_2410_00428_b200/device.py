@@ -1,0 +1,143 @@
+"""Python handle on the sm_100a device half of the C ABI (include/lkv.h).
+
+torch is used only as plumbing: device buffers for K/V/q/out and stream
+wrappers. All data movement and attention run in liblkv.so's kernels and
+copy-engine streams.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+from . import _abi
+from .layersim import KvManager, ModelSpec
+
+DTYPE_BF16, DTYPE_F32 = 0, 1
+
+
+@dataclass
+class DeviceConfig:
+    device: int = 0
+    tp_rank: int = 0
+    tp_size: int = 1
+    pipeline_depth: int = 2
+    gpu_slots: int = 0
+    host_slots: int = 0
+    arena_slots: int = 0
+    max_requests: int = 64
+    max_blocks: int = 4096
+    max_batch: int = 64
+    staging_chunks: int = 4
+    chunk_bytes: int = 16 << 20
+
+    def c(self):
+        return _abi.DeviceConfig(self.device, self.tp_rank, self.tp_size, self.pipeline_depth, self.gpu_slots,
+                                 self.host_slots, self.arena_slots, self.max_requests, self.max_blocks,
+                                 self.max_batch, self.staging_chunks, self.chunk_bytes)
+
+
+def _ptr(t) -> int:
+    return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
+
+
+class Device:
+    """One GPU's KV-head shard of the LayerKV data path, bound to a KvManager."""
+
+    def __init__(self, kv: KvManager, model: ModelSpec, tokens_per_block: int, cfg: DeviceConfig, lib=None):
+        self._lib = lib or _abi.product_lib()
+        if not self._lib.has_device:
+            raise RuntimeError("library has no device half")
+        self.kv = kv  # keep the manager alive while bound
+        self.model = model
+        self.cfg = cfg
+        h = C.c_void_p()
+        self._lib.call("lkv_device_create", C.byref(model.c()), tokens_per_block, C.byref(cfg.c()), C.byref(h))
+        self.handle = h
+        self._lib.call("lkv_device_bind", h, kv.handle)
+        info = _abi.DeviceInfo()
+        self._lib.call("lkv_device_get_info", h, C.byref(info))
+        self.info = info
+        self.slot_bytes = info.slot_bytes
+        self.kv_heads_local = info.kv_heads_local
+        self.q_heads_local = info.q_heads_local
+        self.head_dim = info.head_dim
+        self.tokens_per_block = info.tokens_per_block
+        self.head0 = cfg.tp_rank * info.kv_heads_local
+
+    def close(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self._lib.dll.lkv_device_destroy(h)
+            self.handle = None
+
+    def __del__(self):
+        self.close()
+
+    # ------------------------------------------------------------- streams
+    def torch_stream(self, which: str = "compute"):
+        import torch
+        ptr = {"compute": self.info.compute_stream, "d2h": self.info.d2h_stream, "h2d": self.info.h2d_stream}[which]
+        return torch.cuda.ExternalStream(ptr, device=torch.device("cuda", self.cfg.device))
+
+    def synchronize(self):
+        self._lib.call("lkv_device_synchronize", self.handle)
+
+    def set_timing(self, on: bool):
+        self._lib.call("lkv_device_set_timing", self.handle, int(on))
+
+    # ------------------------------------------------------------- prefill
+    def prefill_layer(self, request_id: int, layer: int, k, v, tokens: int, stream=None):
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        self._lib.call("lkv_prefill_layer", self.handle, request_id, layer, _ptr(k), _ptr(v), tokens, s)
+
+    def prefill_offload_done(self, request_id: int) -> bool:
+        out = C.c_int32()
+        self._lib.call("lkv_device_prefill_offload_done", self.handle, request_id, C.byref(out))
+        return bool(out.value)
+
+    def job_done(self, job_id: int) -> bool:
+        out = C.c_int32()
+        self._lib.call("lkv_device_job_done", self.handle, job_id, C.byref(out))
+        return bool(out.value)
+
+    # ------------------------------------------------------------- decode
+    def decode_begin(self, request_ids):
+        arr = (C.c_int64 * max(1, len(request_ids)))(*request_ids)
+        self._lib.call("lkv_decode_begin", self.handle, arr, len(request_ids))
+
+    def decode_layer(self, layer: int, q, out, scale: float, out_dtype: int = DTYPE_BF16):
+        self._lib.call("lkv_decode_layer", self.handle, layer, _ptr(q), _ptr(out), scale, out_dtype)
+
+    def decode_end(self):
+        self._lib.call("lkv_decode_end", self.handle)
+
+    def decode_stats(self) -> _abi.DecodeStats:
+        s = _abi.DecodeStats()
+        self._lib.call("lkv_decode_last_stats", self.handle, C.byref(s))
+        return s
+
+    def offload_stats(self, reset: bool = False) -> _abi.OffloadStats:
+        s = _abi.OffloadStats()
+        self._lib.call("lkv_offload_last_stats", self.handle, C.byref(s), int(reset))
+        return s
+
+    # ------------------------------------------------------------- synthetic data
+    def fill_kv(self, k, v, tokens: int, token0: int, layer: int, seed: int, stream=None):
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        self._lib.call("lkv_fill_kv", self.handle, _ptr(k), _ptr(v), tokens, token0, layer, seed, s)
+
+    def verify_request(self, request_id: int, n_tokens: int, seed: int) -> int:
+        out = C.c_int64()
+        self._lib.call("lkv_verify_request", self.handle, request_id, n_tokens, seed, C.byref(out))
+        return out.value
+
+    def fill_request(self, request_id: int, n_tokens: int, seed: int):
+        self._lib.call("lkv_fill_request", self.handle, request_id, n_tokens, seed)
+
+    # ------------------------------------------------------------- raw views (tests)
+    def read_host_slot(self, slot: int) -> bytes:
+        """Bytes of one pinned host frame (CPU slot) — the host pool is
+        ordinary pinned memory, readable directly."""
+        self.synchronize()
+        n = self.slot_bytes
+        return C.string_at(self.info.host_pool + slot * n, n)

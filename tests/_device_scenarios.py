@@ -1,0 +1,111 @@
+"""Device-path scenarios shared by __graft_entry__.smoke() and the -m gpu tests.
+
+Each scenario drives the product through the reference call sequence
+(allocate_prefill -> per-layer prefill -> escalation plan/complete -> decode
+iteration) and checks it against the oracle restatement: KV bytes bit-exact
+with the generator wherever they live (GPU slots, pinned host frames, arena),
+attention within 1e-3 relative (fp32 output) of the fp32 CPU restatement.
+"""
+from __future__ import annotations
+
+import math
+
+import numpy as np
+
+from paper_2410_00428_b200 import layersim as ls
+from paper_2410_00428_b200.device import DTYPE_BF16, DTYPE_F32, Device, DeviceConfig
+
+SEED = 0x4C61796572
+REL_TOL = 1e-3       # north star: attention within 1e-3 relative (fp32 accumulate)
+
+
+def gqa_model(L=4, hkv=8, group=4, d=128):
+    return ls.ModelSpec(L, hkv * group, hkv, d, hkv * group * d, 1.0e9, 2)
+
+
+def make(model, bs=16, gpu=512, cpu=512, tp_rank=0, tp_size=1, depth=2, chunk_slots=3, max_blocks=64,
+         max_batch=8, arena=None):
+    kv = ls.KvManager(ls.BlockPools(gpu, cpu, bs), model)
+    slot_bytes = 2 * (model.n_kv_heads // tp_size) * bs * model.d_head * 2
+    cfg = DeviceConfig(device=0, tp_rank=tp_rank, tp_size=tp_size, pipeline_depth=depth, gpu_slots=gpu,
+                       host_slots=cpu, arena_slots=arena or gpu, max_requests=16, max_blocks=max_blocks,
+                       max_batch=max_batch, staging_chunks=4, chunk_bytes=chunk_slots * slot_bytes)
+    dev = Device(kv, model, bs, cfg)
+    return kv, dev
+
+
+def prefill(kv, dev, rid, prompt, x, seed=SEED):
+    """allocate_prefill + per-layer K/V production + lkv_prefill_layer."""
+    import torch
+    assert kv.allocate_prefill(rid, prompt, x)
+    L = dev.model.n_layers
+    k = torch.empty((prompt, dev.kv_heads_local, dev.head_dim), dtype=torch.bfloat16, device="cuda:0")
+    v = torch.empty_like(k)
+    s = dev.torch_stream("compute")
+    for layer in range(L):
+        dev.fill_kv(k, v, prompt, 0, layer, seed, stream=s)
+        dev.prefill_layer(rid, layer, k, v, prompt, stream=s)
+    dev.synchronize()
+
+
+def random_q(n, hq, d, gen_seed):
+    import torch
+    g = torch.Generator(device="cpu").manual_seed(gen_seed)
+    return (torch.rand((n, hq, d), generator=g) * 2 - 1).to(torch.bfloat16)
+
+
+def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=None, tol=None):
+    """One decode iteration over `ids`; every layer compared with the oracle."""
+    import torch
+    import oracle
+    re = oracle.restatement()
+    n = len(ids)
+    hq, d = dev.q_heads_local, dev.head_dim
+    group = hq // dev.kv_heads_local
+    scale = 1.0 / math.sqrt(d)
+    L = dev.model.n_layers
+    qs = [random_q(n, hq, d, 1000 + l) for l in range(L)]
+    outs = []
+    dev.decode_begin(ids)
+    for l in range(L):
+        q = qs[l].to("cuda:0")
+        out = torch.empty((n, hq, d), dtype=torch.float32 if out_dtype == DTYPE_F32 else torch.bfloat16,
+                          device="cuda:0")
+        dev.decode_layer(l, q, out, scale, out_dtype)
+        outs.append(out)
+    dev.decode_end()
+    dev.synchronize()
+    worst = 0.0
+    for l in (layers if layers is not None else range(L)):
+        got = outs[l].float().cpu().numpy()
+        q16 = qs[l].view(torch.int16).numpy().view(np.uint16)
+        for m in range(n):
+            want = re.decode_attn_gen(seed, l, kv_lens[m], dev.head0, dev.kv_heads_local, group, q16[m], scale)
+            err = np.abs(got[m] - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)
+            worst = max(worst, float(err.max()))
+    limit = tol if tol is not None else (REL_TOL if out_dtype == DTYPE_F32 else 8e-3)
+    assert worst <= limit, f"attention rel err {worst:.3e} > {limit}"
+    return worst, outs
+
+
+def smoke_scenario(verbose=False):
+    """Prefill with layer-wise offload + escalation + one decode iteration."""
+    model = gqa_model()
+    kv, dev = make(model)
+    prefill(kv, dev, 0, 100, 2)   # retained {1, 3}: scatter; {0, 2}: pack + D2H
+    prefill(kv, dev, 1, 37, 4)    # all retained
+    prefill(kv, dev, 2, 200, 0)   # all offloaded (multi-chunk D2H)
+    job = kv.plan_offload(1, ls.HALF)  # escalation: gather + D2H of layers {0, 1}
+    assert job is not None and job.job_id >= 0
+    kv.complete_offload(job.job_id)    # waits for the copies, flips the table
+    kv.check_conservation()
+    for rid, n in ((0, 100), (1, 37), (2, 200)):
+        bad = dev.verify_request(rid, n, SEED)
+        assert bad == 0, f"request {rid}: {bad} KV elements differ from the generator"
+    worst, _ = check_attention(dev, [0, 1, 2], [100, 37, 200])
+    st = dev.decode_stats()
+    if verbose:
+        print(f"smoke: bytes bit-exact; attention max rel err {worst:.2e}; "
+              f"h2d {st.h2d_bytes_physical} B in {st.h2d_copies} copies; {st.attn_launches} attention launches")
+    dev.close()
+    return worst
