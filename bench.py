@@ -1,0 +1,439 @@
+"""Benchmark of the B200 LayerKV data path (one JSON line on rank 0).
+
+Metric (BASELINE.json): "KV offload/prefetch GB/s; paged-attn decode HBM GB/s;
+simulated TTFT p50/p99".
+
+Workload (BASELINE.json configs[1], the config the metric is quoted on):
+LLaMA-2-7B shape, 48 GB-capped pools (113,043 GPU blocks), 16k-context
+requests under LayerKV. At 16k the reference's min_retained_layers is 0, so
+every layer of every request is CPU-resident and each decode iteration
+re-fetches all of it (engine.cpp:426-449). The decode batch is what
+max_batch_tokens = 131072 admits: 7 x 16,384 tokens.
+
+  setup : allocate_prefill x 7 (x = 0) and, per layer, the real prefill
+          offload path (pack kernel -> staging -> D2H into the CPU slots'
+          pinned frames) — measured as "offload".
+  step  : one decode iteration through the C ABI: decode_begin (plan_decode_
+          fetch per member, table snapshot), then per layer: H2D prefetch of
+          the layer's 7 x 1024 CPU slots into the arena (copy engine,
+          layer-ahead pipeline) + paged decode attention over it.
+  value : KV bytes the iteration's attention consumed (token-exact, all
+          layers, all ranks) / device time of the K timed steps (max over
+          ranks). Inputs: q in HBM, KV in pinned host frames (their resident
+          place in this config). Each layer streams 1.88 GB > L2 (126 MB).
+  e2e   : the same step with q copied from pinned host memory per layer and
+          the attention output read back to pinned host memory per layer.
+
+`--impl reference`: the reference's path on the host cores — reference
+bookkeeping (oracle/_ref KvManager.plan_decode_fetch when built) plus the
+oracle CPU port executing the booked fetch (memcpy) and fp32 attention on
+all host threads, on a bounded sample (1 request x S layers per step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "KV offload/prefetch GB/s; paged-attn decode HBM GB/s; simulated TTFT p50/p99"
+SEED = 0x4C61796572
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="lkv", choices=["lkv", "reference"])
+    p.add_argument("--ctx", type=int, default=16384)
+    p.add_argument("--batch", type=int, default=7)
+    p.add_argument("--retained", type=int, default=0, help="layers kept on GPU (x); 0 = reference's choice at 16k")
+    p.add_argument("--depth", type=int, default=2, help="prefetch pipeline depth (layers in flight)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-seconds", type=float, default=12.0)
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = max(mx, float(r[2]))
+                for n, v in zip(names, r[5:9]):
+                    if v.lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                continue
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ host link peak
+def host_link_peak(torch, dev):
+    n = 1 << 30
+    h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
+    d = torch.empty(n, dtype=torch.uint8, device=dev)
+    s = torch.cuda.Stream(device=dev)
+    out = {}
+    with torch.cuda.stream(s):
+        for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
+                         ("d2h", lambda: h.copy_(d, non_blocking=True))):
+            fn()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(s)
+            for _ in range(4):
+                fn()
+            e1.record(s)
+            e1.synchronize()
+            out[name] = 4 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9
+    del h, d
+    return out
+
+
+# ------------------------------------------------------------------ CPU port
+def cpu_port(host_pool_ptr, slots_per_layer, slot_bytes, kv_len, hkv, group, bs, d, seconds, max_layers=None):
+    """Oracle CPU port of the decode step (see oracle/cpu_baseline.c)."""
+    import ctypes as C
+    import numpy as np
+    import oracle
+    re = oracle.restatement()
+    fn = re.dll.cpu_decode_layer
+    fn.restype = None
+    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                   C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_int]
+    threads = os.cpu_count() or 1
+    nblk = len(slots_per_layer[0])
+    arena = np.empty(nblk * slot_bytes, np.uint8)
+    q = (np.random.default_rng(0).random((hkv * group, d), dtype=np.float32) * 2 - 1)
+    q16 = (q.view(np.uint32) >> 16).astype(np.uint16)
+    out = np.empty((hkv * group, d), np.float32)
+    rows = [np.asarray(s, np.uint32) for s in slots_per_layer]
+    t0 = time.perf_counter()
+    done = 0
+    while True:  # whole passes over the given layers until the time budget is spent
+        for s in rows:
+            fn(host_pool_ptr, s.ctypes.data, nblk, slot_bytes, kv_len, hkv, group, bs, d, q16.ctypes.data,
+               1.0 / math.sqrt(d), out.ctypes.data, arena.ctypes.data, threads)
+            done += 1
+            if max_layers and done >= max_layers:
+                break
+        if (max_layers and done >= max_layers) or time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    kv_bytes = done * kv_len * 2 * hkv * d * 2
+    return kv_bytes / dt / 1e9, threads, done, dt
+
+
+def reference_arm(args):
+    """`--impl reference`: rank 0 alone runs the reference's CPU path."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import ctypes as C
+    import numpy as np
+    import oracle
+    from paper_2410_00428_b200 import layersim as ls
+    model = ls.llama2_7b()
+    L, bs, d = model.n_layers, 16, model.d_head
+    lib = oracle.ref_lib() if oracle.ref_available() else None
+    kind_book = "reference" if lib is not None else "product"
+    kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model, lib=lib)
+    B = args.batch
+    for rid in range(B):
+        assert kv.allocate_prefill(rid, args.ctx, args.retained)
+    nblk = (args.ctx + bs - 1) // bs
+    slot_bytes = 2 * model.n_kv_heads * bs * d * 2
+    # Host frames: the step reads B x 32 x 1024 distinct slots (60 GB at 16k);
+    # the sample maps them modulo a 4 GiB frame pool (>> LLC, so every read
+    # still comes from DRAM) with synthetic bf16 values.
+    frames = (4 << 30) // slot_bytes
+    pool = np.random.default_rng(1).integers(0x3C00, 0x3F80, size=frames * slot_bytes // 2, dtype=np.uint16)
+    pool[::2] ^= 0x8000
+    tables = []
+    for rid in range(B):
+        r = kv.request(rid)
+        tables.append([[r.blocks[b].layers[l].slot % frames for b in range(nblk)] for l in range(L)])
+    steps = []
+    cores = os.cpu_count() or 1
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        for rid in range(B):  # one decode iteration: every member, every layer
+            jobs = kv.plan_decode_fetch(rid)  # the reference's own booking of this step
+            assert len(jobs) == L - args.retained
+            cpu_port(pool.ctypes.data, tables[rid], slot_bytes, args.ctx, model.n_kv_heads, 1, bs, d, 0.0,
+                     max_layers=L)
+        step = time.perf_counter() - t0
+        if i >= args.warmup:
+            steps.append(step)
+    S = L
+    step_bytes = B * S * args.ctx * ls.kv_bytes_per_token_layer(model)
+    ms = 1000 * statistics.mean(steps)
+    value = step_bytes / (ms / 1000) / 1e9
+    sample = (f"full decode iteration per step ({B} requests x 32 layers x {args.ctx} tokens, 7B shape): "
+              f"{kind_book} bookkeeping (plan_decode_fetch) + oracle CPU port memcpy prefetch + fp32 attention; "
+              f"frames mapped modulo a 4 GiB pool")
+    line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload_config(args),
+            "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(args):
+    return {"workload": (f"config2 LayerKV decode iteration @ {args.ctx // 1024}k context: {args.batch} requests x "
+                         f"{args.ctx} tokens (max_batch_tokens 131072), x={args.retained} retained layers "
+                         f"(reference min_retained_layers), LLaMA-2-7B shape L=32 H=32 Hkv=32 d=128 bs=16, "
+                         f"48 GB-capped pools 113043/904344"),
+            "model_shape": "llama2-7b", "batch": args.batch, "context": args.ctx, "retained_layers": args.retained,
+            "kv_residency": "pinned host frames (CPU slots), prefetched per layer",
+            "l2": "inputs larger than L2 (one layer's KV = 1.88 GB)",
+            "parallelism": f"kv-head tp{args.gpus}", "pipeline_depth": args.depth}
+
+
+# ------------------------------------------------------------------ product arm
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev_t = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev_t)
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+
+    model = ls.llama2_7b()
+    L, bs, d = model.n_layers, 16, model.d_head
+    kvb = ls.kv_bytes_per_token_layer(model)
+    B, ctx, x = args.batch, args.ctx, args.retained
+    nblk = (ctx + bs - 1) // bs
+    kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model)
+    gpu_need = B * nblk * x
+    cpu_need = B * nblk * (L - x)
+    cfg = DeviceConfig(device=local, tp_rank=rank, tp_size=world, pipeline_depth=args.depth,
+                       gpu_slots=max(gpu_need, 1) + 64, host_slots=cpu_need + 64, arena_slots=B * nblk + 16,
+                       max_requests=max(B, 1) + 1, max_blocks=nblk + 8, max_batch=max(B, 1), staging_chunks=4,
+                       chunk_bytes=16 << 20)
+    dev = Device(kv, model, bs, cfg)
+    hl, hql = dev.kv_heads_local, dev.q_heads_local
+    cs = dev.torch_stream("compute")
+    hbm_peak, peak_kind = peaks()
+
+    link = host_link_peak(torch, dev_t)
+
+    # ---------------- setup: real prefill offload of every request (pack + D2H)
+    k = torch.empty((ctx, hl, d), dtype=torch.bfloat16, device=dev_t)
+    v = torch.empty_like(k)
+    dev.offload_stats(reset=True)
+    torch.cuda.synchronize()
+    t_off0 = time.perf_counter()
+    ids = list(range(B))
+    for rid in ids:
+        assert kv.allocate_prefill(rid, ctx, x)
+        for layer in range(L):
+            dev.fill_kv(k, v, ctx, 0, layer, SEED, stream=cs)
+            dev.prefill_layer(rid, layer, k, v, ctx, stream=cs)
+    dev.synchronize()
+    t_off = time.perf_counter() - t_off0
+    ost = dev.offload_stats(reset=True)
+    offload_gbs = ost.d2h_bytes_algorithmic / t_off / 1e9
+    bad = dev.verify_request(B - 1, ctx, SEED)
+
+    # ---------------- decode iteration
+    scale = 1.0 / math.sqrt(d)
+    q = [torch.randn((B, hql, d), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
+    out = [torch.empty((B, hql, d), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
+    gathered = [torch.empty((world * B * hql * d,), dtype=torch.bfloat16, device=dev_t) for _ in range(L)] \
+        if world > 1 else None
+    dev.set_timing(True)
+
+    def step(qsrc=None, outdst=None):
+        dev.decode_begin(ids)
+        for layer in range(L):
+            if qsrc is not None:
+                with torch.cuda.stream(cs):
+                    q[layer].copy_(qsrc[layer], non_blocking=True)
+            dev.decode_layer(layer, q[layer], out[layer], scale, DTYPE_BF16)
+            if world > 1:
+                with torch.cuda.stream(cs):  # the one collective: all-gather of per-head outputs
+                    dist.all_gather_into_tensor(gathered[layer], out[layer].reshape(-1))
+            if outdst is not None:
+                with torch.cuda.stream(cs):
+                    outdst[layer].copy_(out[layer], non_blocking=True)
+        dev.decode_end()
+
+    for _ in range(args.warmup):
+        step()
+    dev.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    attn_ms = h2d_ms = 0.0
+    launches = attn_launches = 0
+    h2d_alg = h2d_phys = kv_read = 0
+    with ClockSampler(local) as clk:
+        e0.record(cs)
+        for _ in range(args.steps):
+            step()
+            st = dev.decode_stats()
+            attn_ms += st.attn_ms
+            h2d_ms += st.h2d_ms
+            launches += st.kernel_launches
+            attn_launches += st.attn_launches
+            h2d_alg += st.h2d_bytes_algorithmic
+            h2d_phys += st.h2d_bytes_physical
+            kv_read += st.kv_bytes_read
+        e1.record(cs)
+        dev.synchronize()
+        torch.cuda.synchronize()
+    elapsed = e0.elapsed_time(e1)
+    if world > 1:
+        t = torch.tensor([elapsed], device=dev_t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+        dist.barrier()
+    total_kv = B * ctx * L * kvb  # token-exact KV bytes consumed per step, all heads (all ranks)
+    value = total_kv * args.steps / (elapsed / 1000) / 1e9
+
+    # ---------------- e2e through the C ABI with host buffers
+    q_host = [t.cpu().pin_memory() for t in q]
+    out_host = [torch.empty((B, hql, d), dtype=torch.bfloat16, pin_memory=True) for _ in range(L)]
+    step(q_host, out_host)
+    dev.synchronize()
+    if world > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step(q_host, out_host)
+        dev.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        t = torch.tensor([e2e_s], device=dev_t, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = total_kv * args.steps / e2e_s / 1e9
+    qbytes = L * B * hql * d * 2
+
+    # ---------------- roofline of the dominant kernel (paged decode attention)
+    per_launch_bytes = B * ctx * kvb // world + 2 * B * hql * d * 2  # KV + q + out
+    avg_launch_ms = attn_ms / max(attn_launches, 1)
+    achieved = per_launch_bytes / (avg_launch_ms / 1000) / 1e9
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "decode_attn_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        r = kv.request(0)
+        slots = [[r.blocks[b].layers[l].slot for b in range(nblk)] for l in range(L)]
+        gbs, cores, done, dt = cpu_port(dev.info.host_pool, slots, dev.slot_bytes, ctx, hl, hql // hl, bs, d,
+                                        args.cpu_seconds)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
+               "sample": f"{done} (request 0, layer) decode passes over the same pinned frames ({ctx} tokens "
+                         f"each, {dt:.1f} s): oracle CPU port memcpy prefetch + fp32 attention, {cores} threads"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": elapsed / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+            "config": workload_config(args),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": achieved / hbm_peak, "traffic": traffic,
+                         "kernel": "decode_attn_kernel (+ split merge)", "peak_kind": peak_kind,
+                         "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms},
+            "host_link": {"prefetch_gbs_per_gpu": h2d_alg / world / (h2d_ms / 1000) / 1e9 if h2d_ms else None,
+                          "prefetch_algorithmic_bytes_per_step": h2d_alg // args.steps * world,
+                          "prefetch_physical_bytes_per_step": h2d_phys // args.steps * world,
+                          "peak_h2d_gbs": link["h2d"], "peak_d2h_gbs": link["d2h"],
+                          "prefetch_frac_of_peak": (h2d_alg / (h2d_ms / 1000) / 1e9) / link["h2d"] if h2d_ms else None,
+                          "offload_gbs_per_gpu": offload_gbs, "offload_frac_of_peak": offload_gbs / link["d2h"],
+                          "offload_bytes": ost.d2h_bytes_algorithmic, "offload_copies": ost.d2h_copies,
+                          "kv_verified_mismatches": bad},
+            "decode_attn_hbm_gbs": achieved,
+            "simulated_ttft": None,
+            "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": qbytes + h2d_phys // args.steps,
+                    "d2h_bytes_per_step": qbytes},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    # pinned tensors used on the device's streams must go before the streams do
+    del q_host, out_host, q, out, k, v, gathered
+    torch.cuda.synchronize()
+    dev.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

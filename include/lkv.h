@@ -289,7 +289,8 @@ typedef struct lkv_decode_stats {
   int64_t h2d_copies;            /* cudaMemcpy(2D)Async calls */
   int64_t kv_bytes_read;         /* token-exact K+V bytes the attention consumed */
   int64_t attn_launches;
-  double attn_ms;                /* summed CUDA-event time of the attention launches */
+  int64_t kernel_launches;       /* every kernel this iteration launched (snapshot, attention, merge) */
+  double attn_ms;               /* summed CUDA-event time of the attention launches */
   double h2d_ms;                 /* CUDA-event span of the prefetch copies */
   double iteration_ms;           /* decode_begin -> decode_end on the device */
 } lkv_decode_stats;
@@ -309,7 +310,7 @@ LKV_API int lkv_offload_last_stats(const lkv_device* dev, lkv_offload_stats* out
  * [tokens][kv_heads_local][head_dim] K and V for tokens [token0, token0+tokens). */
 LKV_API int lkv_fill_kv(lkv_device* dev, void* k, void* v, int64_t tokens, int64_t token0, int32_t layer,
                 uint64_t seed, void* stream);
-/* Counts elements of the request's KV (every layer, tokens < n_tokens) that
+/* Counts 4-byte words of the request's KV (every layer, tokens < n_tokens) that
  * differ from the generator, wherever they live now: GPU slots, or pinned
  * host frames read directly by the kernel. */
 LKV_API int lkv_verify_request(lkv_device* dev, int64_t request_id, int64_t n_tokens, uint64_t seed,

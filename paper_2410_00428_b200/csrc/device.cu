@@ -615,6 +615,7 @@ struct lkv_device final : layersim::KvObserver {
     if (n > 0 && max_nblk > 0) {
       // one launch resolves every layer; layer l's arena stage is l % depth
       dim3 grid((max_nblk + 255) / 256, n, L);
+      dstats.kernel_launches += 1;
       decode_snapshot_kernel<<<grid, 256, 0, cs>>>(d_table, d_seqs, n, cfg.max_blocks, cfg.gpu_slots,
                                                    cfg.arena_slots, cfg.pipeline_depth, d_snap);
       LKV_CUDA(cudaGetLastError());
@@ -674,6 +675,7 @@ struct lkv_device final : layersim::KvObserver {
       }
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;
+      dstats.kernel_launches += n_split > 1 ? 2 : 1;
       if (n_split > 1) {
         decode_merge_kernel<<<n * Hql, D, 0, cs>>>(d_part_o, d_part_ml, n_split, D, out, f32);
         LKV_CUDA(cudaGetLastError());

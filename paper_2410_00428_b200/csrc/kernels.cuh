@@ -406,23 +406,33 @@ __global__ void request_kv_kernel(const int* __restrict__ table_row, int max_blo
   const int e = table_row[static_cast<long long>(l) * max_blocks + b];
   char* slot = e >= 0 ? pool + static_cast<long long>(e) * slot_bytes
                       : host_pool + static_cast<long long>(~e) * slot_bytes;
-  unsigned short* s16 = reinterpret_cast<unsigned short*>(slot);
-  const int per_kv = Hl * bs * D;
+  // 16 B per access: host frames are read/written over the link, where
+  // narrow accesses would be transaction-bound.
+  uint4* s128 = reinterpret_cast<uint4*>(slot);
+  const int vec_row = D / 8;
+  const int per_kv = Hl * bs * vec_row;
   unsigned long long bad = 0;
   for (int i = threadIdx.x; i < 2 * per_kv; i += blockDim.x) {
     const int kvsel = i / per_kv;
     int r = i % per_kv;
-    const int d = r % D;
-    r /= D;
+    const int d0 = (r % vec_row) * 8;
+    r /= vec_row;
     const int t = r % bs;
     const int h = r / bs;
     const long long tok = static_cast<long long>(b) * bs + t;
     if (tok >= n_tokens) continue;
-    const unsigned short want = kv_value_bf16(seed, l, kvsel, tok, head0 + h, d);
-    if (kWrite)
-      s16[i] = want;
-    else
-      bad += (s16[i] != want);
+    unsigned w[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      w[j] = static_cast<unsigned>(kv_value_bf16(seed, l, kvsel, tok, head0 + h, d0 + 2 * j)) |
+             (static_cast<unsigned>(kv_value_bf16(seed, l, kvsel, tok, head0 + h, d0 + 2 * j + 1)) << 16);
+    }
+    if (kWrite) {
+      s128[i] = make_uint4(w[0], w[1], w[2], w[3]);
+    } else {
+      const uint4 got = s128[i];
+      bad += (got.x != w[0]) + (got.y != w[1]) + (got.z != w[2]) + (got.w != w[3]);
+    }
   }
   if (!kWrite) {
     for (int o = 16; o > 0; o >>= 1) bad += __shfl_xor_sync(0xffffffffu, bad, o);
