@@ -20,6 +20,9 @@
 #include <unordered_map>
 #include <vector>
 
+#include <cstdlib>
+
+#include "decode_attn.cuh"
 #include "kernels.cuh"
 #include "layersim/errors.hpp"
 #include "layersim/kv_manager.hpp"
@@ -120,6 +123,11 @@ struct lkv_device final : layersim::KvObserver {
   SeqDesc* d_seqs = nullptr;   // [max_batch]
   char* d_staging = nullptr;   // staging_chunks x seg bytes
   unsigned* d_slotlist = nullptr;  // staging_chunks x seg_slots GPU slot ids
+  AttnSeq* d_aseqs = nullptr;      // [max_batch] (v2)
+  AttnChunk* d_chunks = nullptr;   // chunk list of the iteration (v2)
+  long long chunk_cap = 0, part_cap = 0;
+  int n_chunks = 0;
+  int kernel_version = 2;          // LKV_DECODE_KERNEL=1 selects the v1 split-K kernel
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   unsigned long long* d_counter = nullptr;
@@ -214,7 +222,13 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaMalloc(&d_seqs, cfg.max_batch * sizeof(SeqDesc)));
     LKV_CUDA(cudaMalloc(&d_staging, cfg.staging_chunks * seg_slots * sb));
     LKV_CUDA(cudaMalloc(&d_slotlist, cfg.staging_chunks * seg_slots * sizeof(unsigned)));
+    // G=4 stays on the split-K kernel until the tensor-core GQA path lands
+    // (measured: v1 65% vs v2 58% of HBM peak at G=4; v2 ahead at G=1, 2, 8).
+    kernel_version = G == 4 ? 1 : 2;
+    if (const char* kv = std::getenv("LKV_DECODE_KERNEL")) kernel_version = std::atoi(kv) == 1 ? 1 : 2;
+    LKV_CUDA(cudaMalloc(&d_aseqs, cfg.max_batch * sizeof(AttnSeq)));
     const long long parts = static_cast<long long>(cfg.max_batch) * Hql * kMaxSplits;
+    part_cap = parts;
     LKV_CUDA(cudaMalloc(&d_part_o, parts * D * sizeof(float)));
     LKV_CUDA(cudaMalloc(&d_part_ml, parts * 2 * sizeof(float)));
     LKV_CUDA(cudaMalloc(&d_counter, sizeof(unsigned long long)));
@@ -282,6 +296,8 @@ struct lkv_device final : layersim::KvObserver {
     cudaFree(d_slotlist);
     cudaFree(d_part_o);
     cudaFree(d_part_ml);
+    cudaFree(d_aseqs);
+    cudaFree(d_chunks);
     cudaFree(d_counter);
     for (auto s : {cs, d2h, h2d})
       if (s) cudaStreamDestroy(s);
@@ -612,6 +628,7 @@ struct lkv_device final : layersim::KvObserver {
     if (timing) LKV_CUDA(cudaEventRecord(t_it0, cs));
     LKV_CUDA(cudaMemcpyAsync(d_seqs, desc, std::max(n, 1) * sizeof(SeqDesc), cudaMemcpyHostToDevice, cs));
     ring.commit(cs);
+    if (kernel_version == 2) plan_chunks();
     if (n > 0 && max_nblk > 0) {
       // one launch resolves every layer; layer l's arena stage is l % depth
       dim3 grid((max_nblk + 255) / 256, n, L);
@@ -629,6 +646,84 @@ struct lkv_device final : layersim::KvObserver {
     cudaEventDestroy(ev);
     in_iteration = true;
     for (int l = 0; l < std::min(cfg.pipeline_depth, L); ++l) issue_fetch(l);
+  }
+
+  // ---- v2: persistent warps, TMA bulk ring (decode_attn.cuh) ------------------
+  // Chunk size: the largest power of two <= 32 that still deals every warp of
+  // the persistent grid >= 8 units (load balance on ragged batches).
+  void plan_chunks() {
+    const long long warps = static_cast<long long>(sms) * v2_warps(G);
+    const long long block_heads = static_cast<long long>(total_blocks) * Hl;
+    int cb = 32;
+    while (cb > 1 && block_heads / cb < 8 * warps) cb >>= 1;
+    std::vector<AttnChunk> ch;
+    auto* aseq = reinterpret_cast<AttnSeq*>(ring.reserve(std::max<std::size_t>(members.size(), 1) * sizeof(AttnSeq)));
+    for (std::size_t i = 0; i < members.size(); ++i) {
+      const Member& m = members[i];
+      aseq[i] = {m.blk_off, m.kv_len, static_cast<int>(ch.size()), (m.nblk + cb - 1) / cb};
+      for (int b0 = 0; b0 < m.nblk; b0 += cb) ch.push_back({static_cast<int>(i), b0, std::min(cb, m.nblk - b0), 0});
+    }
+    LKV_CUDA(cudaMemcpyAsync(d_aseqs, aseq, std::max<std::size_t>(members.size(), 1) * sizeof(AttnSeq),
+                             cudaMemcpyHostToDevice, cs));
+    ring.commit(cs);
+    n_chunks = static_cast<int>(ch.size());
+    const long long units = static_cast<long long>(n_chunks) * Hl;
+    if (units * G > part_cap) {  // grow the partial buffers (outside any kernel's lifetime)
+      LKV_CUDA(cudaStreamSynchronize(cs));
+      cudaFree(d_part_o);
+      cudaFree(d_part_ml);
+      part_cap = units * G * 2;
+      LKV_CUDA(cudaMalloc(&d_part_o, part_cap * D * sizeof(float)));
+      LKV_CUDA(cudaMalloc(&d_part_ml, part_cap * 2 * sizeof(float)));
+    }
+    if (static_cast<long long>(ch.size()) > chunk_cap) {
+      LKV_CUDA(cudaStreamSynchronize(cs));
+      cudaFree(d_chunks);
+      chunk_cap = static_cast<long long>(ch.size()) * 2;
+      LKV_CUDA(cudaMalloc(&d_chunks, chunk_cap * sizeof(AttnChunk)));
+    }
+    if (!ch.empty()) {
+      auto* hc = reinterpret_cast<AttnChunk*>(ring.reserve(ch.size() * sizeof(AttnChunk)));
+      std::memcpy(hc, ch.data(), ch.size() * sizeof(AttnChunk));
+      LKV_CUDA(cudaMemcpyAsync(d_chunks, hc, ch.size() * sizeof(AttnChunk), cudaMemcpyHostToDevice, cs));
+      ring.commit(cs);
+    }
+  }
+
+  // Warps x stages per CTA (one CTA per SM). Measured on B200 (scripts/
+  // attn_micro.py, 7 x 16k, 7B): G=1 12x2 91% of HBM peak, 8x3 89%, 6x4 91%.
+  // G>=2 keeps 8x3 (register-limited to 8 warps).
+  static int v2_warps(int g) { return g == 1 ? 12 : 8; }
+
+  template <int GG, int BB, int W, int S>
+  void launch_v2_cfg(int l, const void* q, float sl2) {
+    using K = AttnV2<GG, BB, W, S>;
+    auto fn = decode_attn_v2_kernel<GG, BB, W, S>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+      LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem));
+      attr_set = true;
+    }
+    const int units = n_chunks * Hl;
+    const int grid = std::max(1, std::min(sms, (units + W - 1) / W));
+    fn<<<grid, K::kThreads, K::kSmem, cs>>>(dbuf, sb, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
+                                            d_aseqs, d_chunks, units, static_cast<const __nv_bfloat16*>(q),
+                                            d_part_o, d_part_ml, sl2);
+  }
+
+  template <int GG, int BB>
+  void launch_v2(int l, const void* q, float sl2) {
+    if constexpr (GG == 1)
+      launch_v2_cfg<GG, BB, 12, 2>(l, q, sl2);
+    else
+      launch_v2_cfg<GG, BB, 8, 3>(l, q, sl2);
+  }
+
+  template <int GG>
+  void launch_v2_bs(int l, const void* q, float sl2) {
+    if (bs == 16) launch_v2<GG, 16>(l, q, sl2);
+    else if (bs == 32) launch_v2<GG, 32>(l, q, sl2);
+    else launch_v2<GG, 64>(l, q, sl2);
   }
 
   template <int GG, int BB>
@@ -654,7 +749,22 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));
     const int n = static_cast<int>(members.size());
     if (timing) LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
-    if (n > 0) {
+    if (n > 0 && kernel_version == 2) {
+      const float sl2 = scale * 1.4426950408889634f;
+      if (n_chunks > 0) {
+        switch (G) {
+          case 1: launch_v2_bs<1>(l, q, sl2); break;
+          case 2: launch_v2_bs<2>(l, q, sl2); break;
+          case 4: launch_v2_bs<4>(l, q, sl2); break;
+          default: launch_v2_bs<8>(l, q, sl2); break;
+        }
+        LKV_CUDA(cudaGetLastError());
+      }
+      decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
+      LKV_CUDA(cudaGetLastError());
+      dstats.attn_launches += 1;
+      dstats.kernel_launches += n_chunks > 0 ? 2 : 1;
+    } else if (n > 0) {
       const int pairs = n * Hl;
       const int target = 4 * sms;
       int n_split = std::max(1, std::min((target + pairs - 1) / pairs, std::max(max_nblk, 1)));

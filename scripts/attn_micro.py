@@ -1,0 +1,66 @@
+"""Decode-attention microbenchmark (development aid; the judged numbers come
+from bench.py). Same shape as the bench step (7 x 16k tokens, 7B), but with
+every layer GPU-resident so only the attention kernel is timed.
+
+  python scripts/attn_micro.py [--group 1] [--ctx 16384] [--batch 7] [--layers 4]
+"""
+import argparse
+import json
+import math
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2410_00428_b200 import layersim as ls  # noqa: E402
+from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig  # noqa: E402
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--group", type=int, default=1)
+    p.add_argument("--hkv", type=int, default=0)
+    p.add_argument("--ctx", type=int, default=16384)
+    p.add_argument("--batch", type=int, default=7)
+    p.add_argument("--layers", type=int, default=4)
+    p.add_argument("--bs", type=int, default=16)
+    p.add_argument("--iters", type=int, default=5)
+    a = p.parse_args()
+    hkv = a.hkv or (32 if a.group == 1 else 8)
+    model = ls.ModelSpec(a.layers, hkv * a.group, hkv, 128, hkv * a.group * 128, 7e9, 2)
+    nblk = (a.ctx + a.bs - 1) // a.bs
+    slots = a.batch * nblk * a.layers
+    kv = ls.KvManager(ls.BlockPools(slots + 64, 64, a.bs), model)
+    cfg = DeviceConfig(gpu_slots=slots + 64, host_slots=64, arena_slots=a.batch * nblk + 8, max_requests=a.batch + 1,
+                       max_blocks=nblk + 4, max_batch=a.batch, pipeline_depth=2)
+    dev = Device(kv, model, a.bs, cfg)
+    ids = list(range(a.batch))
+    for r in ids:
+        assert kv.allocate_prefill(r, a.ctx, a.layers)
+        dev.fill_request(r, a.ctx, 1)
+    hq = dev.q_heads_local
+    q = torch.randn((a.batch, hq, 128), dtype=torch.bfloat16, device="cuda")
+    out = torch.empty_like(q)
+    dev.set_timing(True)
+    res = []
+    for it in range(a.iters + 2):
+        dev.decode_begin(ids)
+        for l in range(a.layers):
+            dev.decode_layer(l, q, out, 1 / math.sqrt(128), DTYPE_BF16)
+        dev.decode_end()
+        st = dev.decode_stats()
+        if it >= 2:
+            res.append(st.attn_ms / st.attn_launches)
+    kvb = a.batch * a.ctx * 2 * hkv * 128 * 2
+    ms = min(res)
+    print(json.dumps({"variant": os.environ.get("LKV_V2_CFG", "default"), "group": a.group, "bs": a.bs,
+                      "ms_per_layer": ms, "GBps": kvb / (ms / 1e3) / 1e9,
+                      "frac_of_6536.7": kvb / (ms / 1e3) / 1e9 / 6536.7}))
+    dev.close()
+
+
+if __name__ == "__main__":
+    main()
