@@ -119,11 +119,18 @@ class KvObserver {
                                    bool orphaned, const RequestKv* kv) = 0;
   // Called BEFORE the request's slots return to the free lists.
   virtual void on_release(std::int64_t request_id, const RequestKv& kv) = 0;
+  // The manager is going away: drop every pointer into it.
+  virtual void on_manager_destroyed() {}
 };
 
 class KvManager {
  public:
   KvManager(BlockPools pools, const ModelSpec& model);
+  ~KvManager() {
+    if (observer_) observer_->on_manager_destroyed();
+  }
+  KvManager(const KvManager&) = default;
+  KvManager& operator=(const KvManager&) = default;
 
   int tokens_per_block() const { return pools_.tokens_per_block; }
   std::int64_t gpu_blocks_total() const { return pools_.gpu_blocks_total; }

@@ -23,6 +23,7 @@
 #include <cstdlib>
 
 #include "decode_attn.cuh"
+#include "decode_gqa_tc.cuh"
 #include "kernels.cuh"
 #include "layersim/errors.hpp"
 #include "layersim/kv_manager.hpp"
@@ -127,7 +128,11 @@ struct lkv_device final : layersim::KvObserver {
   AttnChunk* d_chunks = nullptr;   // chunk list of the iteration (v2)
   long long chunk_cap = 0, part_cap = 0;
   int n_chunks = 0;
-  int kernel_version = 2;          // LKV_DECODE_KERNEL=1 selects the v1 split-K kernel
+  // 1 = split-K CUDA-core kernel, 2 = persistent CUDA-core kernel fed by TMA
+  // bulk copies (decode_attn.cuh), 3 = tcgen05 GQA tile (decode_gqa_tc.cuh).
+  // LKV_DECODE_KERNEL overrides the per-group-size default.
+  int kernel_version = 2;
+  CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
   unsigned long long* d_counter = nullptr;
@@ -222,10 +227,20 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaMalloc(&d_seqs, cfg.max_batch * sizeof(SeqDesc)));
     LKV_CUDA(cudaMalloc(&d_staging, cfg.staging_chunks * seg_slots * sb));
     LKV_CUDA(cudaMalloc(&d_slotlist, cfg.staging_chunks * seg_slots * sizeof(unsigned)));
-    // G=4 stays on the split-K kernel until the tensor-core GQA path lands
-    // (measured: v1 65% vs v2 58% of HBM peak at G=4; v2 ahead at G=1, 2, 8).
-    kernel_version = G == 4 ? 1 : 2;
-    if (const char* kv = std::getenv("LKV_DECODE_KERNEL")) kernel_version = std::atoi(kv) == 1 ? 1 : 2;
+    // G >= 2: the group's QK^T / PV are dense enough that CUDA cores fall
+    // behind HBM (32k x 16, scripts/attn_micro.py: v2 85/70/39% of peak at
+    // G=2/4/8) -> tcgen05 tile (95/93/89%).
+    kernel_version = G >= 2 ? 3 : 2;
+    if (const char* kv = std::getenv("LKV_DECODE_KERNEL")) {
+      const int v = std::atoi(kv);
+      kernel_version = (v == 1 || v == 3) ? v : 2;
+    }
+    {
+      const unsigned long long rows = static_cast<unsigned long long>(std::max<long long>(frames, 1)) * 2 * Hl * bs;
+      if (rows > 0x7FFFFFFFull) throw CapacityError("pool + arena rows exceed the TMA coordinate range");
+      if (!tc::make_map_2d(&kvmap, dbuf, D, rows, static_cast<uint64_t>(D) * 2, 64, bs, true))
+        throw CudaError("cuTensorMapEncodeTiled failed for the KV pool map");
+    }
     LKV_CUDA(cudaMalloc(&d_aseqs, cfg.max_batch * sizeof(AttnSeq)));
     const long long parts = static_cast<long long>(cfg.max_batch) * Hql * kMaxSplits;
     part_cap = parts;
@@ -366,6 +381,8 @@ struct lkv_device final : layersim::KvObserver {
       journal.push_back({tindex(row, l, b), enc(e), 0});
     }
   }
+
+  void on_manager_destroyed() override { kv = nullptr; }
 
   void on_release(std::int64_t id, const RequestKv&) override {
     auto it = row_of.find(id);
@@ -628,7 +645,7 @@ struct lkv_device final : layersim::KvObserver {
     if (timing) LKV_CUDA(cudaEventRecord(t_it0, cs));
     LKV_CUDA(cudaMemcpyAsync(d_seqs, desc, std::max(n, 1) * sizeof(SeqDesc), cudaMemcpyHostToDevice, cs));
     ring.commit(cs);
-    if (kernel_version == 2) plan_chunks();
+    if (kernel_version >= 2) plan_chunks();
     if (n > 0 && max_nblk > 0) {
       // one launch resolves every layer; layer l's arena stage is l % depth
       dim3 grid((max_nblk + 255) / 256, n, L);
@@ -651,11 +668,16 @@ struct lkv_device final : layersim::KvObserver {
   // ---- v2: persistent warps, TMA bulk ring (decode_attn.cuh) ------------------
   // Chunk size: the largest power of two <= 32 that still deals every warp of
   // the persistent grid >= 8 units (load balance on ragged batches).
+  // The tensor-core kernel deals units to CTAs instead of warps and works in
+  // 128-token tiles: chunks of up to 16 tiles, never below one tile.
   void plan_chunks() {
-    const long long warps = static_cast<long long>(sms) * v2_warps(G);
+    const bool tc_path = kernel_version == 3;
+    const long long workers = static_cast<long long>(sms) * (tc_path ? 1 : v2_warps(G));
     const long long block_heads = static_cast<long long>(total_blocks) * Hl;
-    int cb = 32;
-    while (cb > 1 && block_heads / cb < 8 * warps) cb >>= 1;
+    const int tile_blocks = 128 / bs;
+    int cb = tc_path ? 16 * tile_blocks : 32;
+    const int cb_min = tc_path ? tile_blocks : 1;
+    while (cb > cb_min && block_heads / cb < 8 * workers) cb >>= 1;
     std::vector<AttnChunk> ch;
     auto* aseq = reinterpret_cast<AttnSeq*>(ring.reserve(std::max<std::size_t>(members.size(), 1) * sizeof(AttnSeq)));
     for (std::size_t i = 0; i < members.size(); ++i) {
@@ -694,6 +716,31 @@ struct lkv_device final : layersim::KvObserver {
   // attn_micro.py, 7 x 16k, 7B): G=1 12x2 91% of HBM peak, 8x3 89%, 6x4 91%.
   // G>=2 keeps 8x3 (register-limited to 8 warps).
   static int v2_warps(int g) { return g == 1 ? 12 : 8; }
+
+  // ---- v3: tcgen05 GQA tile (decode_gqa_tc.cuh) -------------------------------
+  template <int GG, int BB>
+  void launch_tc(int l, const void* q, float sl2) {
+    constexpr int NS = 3;
+    using K = GqaTc<GG, BB, NS>;
+    auto fn = decode_gqa_tc_kernel<GG, BB, NS>;
+    static bool attr_set = false;  // per instantiation
+    if (!attr_set) {
+      LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem));
+      attr_set = true;
+    }
+    const int units = n_chunks * Hl;
+    const int grid = std::max(1, std::min(sms, units));
+    fn<<<grid, K::kThreads, K::kSmem, cs>>>(kvmap, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
+                                            d_aseqs, d_chunks, units, static_cast<const __nv_bfloat16*>(q),
+                                            d_part_o, d_part_ml, sl2);
+  }
+
+  template <int GG>
+  void launch_tc_bs(int l, const void* q, float sl2) {
+    if (bs == 16) launch_tc<GG, 16>(l, q, sl2);
+    else if (bs == 32) launch_tc<GG, 32>(l, q, sl2);
+    else launch_tc<GG, 64>(l, q, sl2);
+  }
 
   template <int GG, int BB, int W, int S>
   void launch_v2_cfg(int l, const void* q, float sl2) {
@@ -749,9 +796,17 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));
     const int n = static_cast<int>(members.size());
     if (timing) LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
-    if (n > 0 && kernel_version == 2) {
+    if (n > 0 && kernel_version >= 2) {
       const float sl2 = scale * 1.4426950408889634f;
-      if (n_chunks > 0) {
+      if (n_chunks > 0 && kernel_version == 3) {
+        switch (G) {
+          case 1: launch_tc_bs<1>(l, q, sl2); break;
+          case 2: launch_tc_bs<2>(l, q, sl2); break;
+          case 4: launch_tc_bs<4>(l, q, sl2); break;
+          default: launch_tc_bs<8>(l, q, sl2); break;
+        }
+        LKV_CUDA(cudaGetLastError());
+      } else if (n_chunks > 0) {
         switch (G) {
           case 1: launch_v2_bs<1>(l, q, sl2); break;
           case 2: launch_v2_bs<2>(l, q, sl2); break;

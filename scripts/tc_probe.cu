@@ -69,7 +69,7 @@ __global__ void __launch_bounds__(128, 1)
     } else {
       tx = 32768;
       bar_expect_tx(&s.bar_tma, tx);
-      for (int h = 0; h < 2; ++h) tma_load_2d(s.b + h * 16384, &mapB, h * 64, 0, &s.bar_tma);
+      for (int h = 0; h < 2; ++h) tma_load_2d(s.b + h * 16384, &mapA, h * 64, 0, &s.bar_tma);
     }
   }
   // manual operands

@@ -92,6 +92,21 @@ def test_attention_parity_ragged(group, bs):
     sc.check_attention(dev, list(range(len(lens))), lens)
 
 
+@pytest.mark.parametrize("kernel", [1, 2, 3])
+@pytest.mark.parametrize("group,bs", [(1, 16), (2, 32), (4, 16), (8, 16), (8, 64)])
+def test_attention_parity_each_kernel(kernel, group, bs, monkeypatch):
+    """Every decode kernel (split-K CUDA core, persistent TMA-bulk CUDA core,
+    tcgen05 GQA tile) against the fp32 oracle on ragged lengths, including
+    chunks that end mid-tile and a sequence longer than one chunk."""
+    monkeypatch.setenv("LKV_DECODE_KERNEL", str(kernel))
+    model = sc.gqa_model(L=2, hkv=4, group=group)
+    kv, dev = sc.make(model, bs=bs, gpu=4000, cpu=4000, max_blocks=640, arena=4000)
+    lens = [1, 100, 129, 2 * bs + 3, 5000]
+    for rid, n in enumerate(lens):
+        sc.prefill(kv, dev, rid, n, rid % 3)
+    sc.check_attention(dev, list(range(len(lens))), lens)
+
+
 def test_attention_bf16_output():
     model = sc.gqa_model(L=2, hkv=8, group=4)
     kv, dev = sc.make(model)
