@@ -262,6 +262,16 @@ LKV_API int lkv_device_synchronize(lkv_device* dev);
  * stream) via an event. */
 LKV_API int lkv_prefill_layer(lkv_device* dev, int64_t request_id, int32_t layer, const void* k,
                       const void* v, int64_t tokens, void* stream);
+/* Causal GQA prefill attention of one layer on the tcgen05 tensor cores —
+ * the per-layer compute that schedule_prefill_span charges as prefill_time/L
+ * (engine.cpp:27-28, cost_model.cpp:39-44) and that a layer's offload D2H
+ * hides behind. q [tokens][q_heads_local][head_dim], k/v
+ * [tokens][kv_heads_local][head_dim], out [tokens][q_heads_local][head_dim],
+ * bf16 on the device, out in out_dtype (LKV_DTYPE_BF16 for serving,
+ * LKV_DTYPE_F32 for parity checks); query row i attends keys 0..i. Runs on
+ * `stream` (NULL = compute stream). */
+LKV_API int lkv_prefill_attention(lkv_device* dev, const void* q, const void* k, const void* v, void* out,
+                                  int64_t tokens, float scale, int32_t out_dtype, void* stream);
 /* 1 when the D2H copies of an escalation job have drained. */
 LKV_API int lkv_device_job_done(lkv_device* dev, int64_t job_id, int32_t* done);
 /* 1 when every prefill-layer D2H issued so far for this request has drained. */

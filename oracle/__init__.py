@@ -89,6 +89,9 @@ class Restatement:
         d.oracle_decode_attn_gen.restype = None
         d.oracle_decode_attn_gen.argtypes = [C.c_uint64, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int,
                                              C.c_void_p, C.c_float, C.c_void_p]
+        d.oracle_prefill_attn.restype = None
+        d.oracle_prefill_attn.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int, C.c_int, C.c_int,
+                                          C.c_float, C.c_void_p]
         self.dll = d
 
     # numpy helpers -------------------------------------------------------
@@ -124,6 +127,18 @@ class Restatement:
         out = np.empty((hq, d), np.float32)
         self.dll.oracle_decode_attn(q.ctypes.data, k.ctypes.data, v.ctypes.data, kv_len, hq, hkv, d, scale,
                                     out.ctypes.data)
+        return out
+
+    def prefill_attn(self, q, k, v, scale):
+        """Causal attention, q [T][hq][d], k/v [T][hkv][d] (bf16 bits) -> fp32 [T][hq][d]."""
+        import numpy as np
+        q = np.ascontiguousarray(q, np.uint16)
+        k = np.ascontiguousarray(k, np.uint16)
+        v = np.ascontiguousarray(v, np.uint16)
+        T, hq, d = q.shape
+        out = np.empty((T, hq, d), np.float32)
+        self.dll.oracle_prefill_attn(q.ctypes.data, k.ctypes.data, v.ctypes.data, T, hq, k.shape[1], d, scale,
+                                     out.ctypes.data)
         return out
 
     def decode_attn_gen(self, seed, layer, kv_len, head0, hkv_local, group, q, scale):

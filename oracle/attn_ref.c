@@ -68,3 +68,35 @@ void oracle_decode_attn_gen(uint64_t seed, int layer, int64_t kv_len, int head0,
   free(k);
   free(v);
 }
+
+/* Causal prefill attention (no reference arithmetic either):
+ * q [tokens][hq][d], k/v [tokens][hkv][d] bf16 bits, out [tokens][hq][d] fp32;
+ * query row i of head h attends keys 0..i of kv head h / (hq/hkv). */
+void oracle_prefill_attn(const uint16_t* q, const uint16_t* k, const uint16_t* v, int64_t tokens, int hq,
+                         int hkv, int d, float scale, float* out) {
+  const int g = hq / hkv;
+  double* s = (double*)malloc(sizeof(double) * (size_t)(tokens > 0 ? tokens : 1));
+  double* o = (double*)malloc(sizeof(double) * (size_t)d);
+  for (int64_t i = 0; i < tokens; ++i)
+    for (int h = 0; h < hq; ++h) {
+      const int kh = h / g;
+      double m = -INFINITY;
+      for (int64_t t = 0; t <= i; ++t) {
+        double acc = 0.0;
+        for (int e = 0; e < d; ++e)
+          acc += (double)bf16_to_f32(q[(i * hq + h) * d + e]) * (double)bf16_to_f32(k[(t * hkv + kh) * d + e]);
+        s[t] = acc * scale;
+        if (s[t] > m) m = s[t];
+      }
+      double l = 0.0;
+      for (int e = 0; e < d; ++e) o[e] = 0.0;
+      for (int64_t t = 0; t <= i; ++t) {
+        const double p = exp(s[t] - m);
+        l += p;
+        for (int e = 0; e < d; ++e) o[e] += p * (double)bf16_to_f32(v[(t * hkv + kh) * d + e]);
+      }
+      for (int e = 0; e < d; ++e) out[(i * hq + h) * d + e] = (float)(o[e] / l);
+    }
+  free(s);
+  free(o);
+}

@@ -152,6 +152,7 @@ _PROTOS = {
     "lkv_device_bind": [vp, vp],
     "lkv_device_synchronize": [vp],
     "lkv_prefill_layer": [vp, i64, i32, vp, vp, i64, vp],
+    "lkv_prefill_attention": [vp, vp, vp, vp, vp, i64, f32, i32, vp],
     "lkv_device_job_done": [vp, i64, P(i32)],
     "lkv_device_prefill_offload_done": [vp, i64, P(i32)],
     "lkv_decode_begin": [vp, P(i64), i32],
@@ -166,7 +167,7 @@ _PROTOS = {
 }
 _RET = {"lkv_last_error": C.c_char_p, "lkv_version": C.c_char_p}
 
-DEVICE_SYMBOLS = [n for n in _PROTOS if n.startswith(("lkv_device", "lkv_prefill_layer", "lkv_decode_begin",
+DEVICE_SYMBOLS = [n for n in _PROTOS if n.startswith(("lkv_device", "lkv_prefill_layer", "lkv_prefill_attention", "lkv_decode_begin",
                                                      "lkv_decode_layer", "lkv_decode_end", "lkv_decode_last",
                                                      "lkv_offload_last", "lkv_fill", "lkv_verify"))]
 ALL_SYMBOLS = list(_PROTOS) + list(_RET)

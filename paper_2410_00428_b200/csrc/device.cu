@@ -24,6 +24,7 @@
 
 #include "decode_attn.cuh"
 #include "decode_gqa_tc.cuh"
+#include "prefill_attn.cuh"
 #include "kernels.cuh"
 #include "layersim/errors.hpp"
 #include "layersim/kv_manager.hpp"
@@ -942,6 +943,33 @@ int lkv_prefill_layer(lkv_device* d, int64_t id, int32_t layer, const void* k, c
   LKV_REQUIRE(d && k && v && tokens >= 0 && d->kv);
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
   d->prefill_layer(id, layer, k, v, tokens, static_cast<cudaStream_t>(stream));
+  LKV_CATCH
+}
+
+int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const void* v, void* out, int64_t tokens,
+                          float scale, int32_t out_dtype, void* stream) {
+  LKV_REQUIRE(d && q && k && v && out && tokens >= 0);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  if (tokens == 0) return LKV_OK;
+  if (tokens > 0x7FFFFF80ll) throw std::invalid_argument("prefill_attention: too many tokens");
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->cs;
+  const uint64_t T = static_cast<uint64_t>(tokens), D = static_cast<uint64_t>(d->D);
+  CUtensorMap qm, km, vm;
+  if (!tc::make_map_3d(&qm, q, D, d->Hql, T, D * 2, D * 2 * d->Hql, 64, 1, 128, true) ||
+      !tc::make_map_3d(&km, k, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true) ||
+      !tc::make_map_3d(&vm, v, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true))
+    throw CudaError("prefill_attention: cuTensorMapEncodeTiled failed (pointers must be 16 B aligned)");
+  static bool attr_set = false;
+  if (!attr_set) {
+    LKV_CUDA(cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  PrefillAttnSmem::kBytes));
+    attr_set = true;
+  }
+  const dim3 grid(static_cast<unsigned>((tokens + 127) / 128), static_cast<unsigned>(d->Hql));
+  prefill_attn_kernel<<<grid, PrefillAttnSmem::kThreads, PrefillAttnSmem::kBytes, s>>>(
+      qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
+      scale * 1.4426950408889634f);
+  LKV_CUDA(cudaGetLastError());
   LKV_CATCH
 }
 

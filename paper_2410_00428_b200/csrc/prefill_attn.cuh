@@ -1,0 +1,258 @@
+// Causal GQA prefill attention on tcgen05: the
+// per-layer compute that a layer's offload D2H hides behind
+// (engine.cpp:27-31, schedule_prefill_span). The only place on the path where
+// the work is a dense contraction, so the only tensor-core kernel besides the
+// GQA decode tile.
+//
+// One CTA per (128-row query tile, query head), heaviest (diagonal-farthest)
+// tiles first. 192 threads:
+//   warp 0     TMA producer: Q tile once, then K/V tiles {64 d, 1 head, 128 tok}
+//              through 3D tensor maps over [tokens][heads][128] (swizzle-128B,
+//              out-of-range tokens zero-filled) into a 2-stage ring;
+//   warp 1     MMA issuer + TMEM owner. S(j) = Q K_j^T (M=N=128, K=128) into
+//              one of two TMEM S buffers; S(j+1) is issued as soon as K_{j+1}
+//              lands, so QK^T overlaps the softmax of tile j. O += P_j V_j
+//              accumulates in TMEM (P from smem K-major, V MN-major);
+//   warps 2-5  softmax: thread = query row = TMEM lane, the whole 128-column
+//              row in registers. Lazy rescaling: the running max only moves
+//              when a tile exceeds it by more than 2^8, then the warp
+//              rescales its O rows in TMEM (ld/scale/st) before handing the
+//              next P over. P = hi + lo in bf16 (two MMAs into the same O):
+//              ~2^-16 relative, inside the 1e-3 parity bar.
+// TMEM: S0 [0,128) S1 [128,256) O [256,384) of a 512-column allocation.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "tc_sm100.cuh"
+
+namespace lkv {
+
+struct PrefillAttnSmem {
+  static constexpr int kQ = 0;               // 32 KiB: 2 SW128 halves (d 0-63, 64-127)
+  static constexpr int kKV = 32768;          // 2 stages x (K 32 KiB | V 32 KiB)
+  static constexpr int kStage = 65536;
+  static constexpr int kPhi = kKV + 2 * kStage;  // 32 KiB: 2 halves (tok 0-63, 64-127)
+  static constexpr int kPlo = kPhi + 32768;
+  static constexpr int kBar = kPlo + 32768;      // mbarriers
+  static constexpr int kNumBars = 12;
+  static constexpr int kTmem = kBar + kNumBars * 8;
+  static constexpr int kBytes = kTmem + 16 + 1024;  // + alignment slack
+  static constexpr int kThreads = 192;
+  static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
+};
+
+__device__ __forceinline__ void prefill_named_bar(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+__global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
+    const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+    const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
+    float scale_log2) {
+  using S = PrefillAttnSmem;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::kBar);
+  uint64_t* q_full = bars;
+  uint64_t* kv_full = bars + 1;   // [2]
+  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* s_full = bars + 5;    // [2]
+  uint64_t* s_empty = bars + 7;   // [2]
+  uint64_t* p_full = bars + 9;
+  uint64_t* o_full = bars + 10;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S::kTmem);
+
+  const int nq = (tokens + 127) / 128;
+  const int qt = nq - 1 - static_cast<int>(blockIdx.x);
+  const int hq = blockIdx.y, h = hq / G;
+  const int nt = qt + 1;  // causal: KV tiles 0..qt
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tc::bar_init(q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::bar_init(&kv_full[b], 1);
+      tc::bar_init(&kv_empty[b], 1);
+      tc::bar_init(&s_full[b], 1);
+      tc::bar_init(&s_empty[b], 128);
+    }
+    tc::bar_init(p_full, 128);
+    tc::bar_init(o_full, 1);
+    tc::bar_fence_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&qmap);
+      tc::tma_prefetch_desc(&kmap);
+      tc::tma_prefetch_desc(&vmap);
+      tc::bar_expect_tx(q_full, 32768);
+      tc::tma_load_3d(sm + S::kQ, &qmap, 0, hq, qt * 128, q_full);
+      tc::tma_load_3d(sm + S::kQ + 16384, &qmap, 64, hq, qt * 128, q_full);
+      for (int j = 0; j < nt; ++j) {
+        const int st = j & 1;
+        tc::bar_wait(&kv_empty[st], ((j >> 1) & 1u) ^ 1u);
+        tc::bar_expect_tx(&kv_full[st], 65536);
+        uint8_t* kt = sm + S::kKV + st * S::kStage;
+        tc::tma_load_3d(kt, &kmap, 0, h, j * 128, &kv_full[st]);
+        tc::tma_load_3d(kt + 16384, &kmap, 64, h, j * 128, &kv_full[st]);
+        tc::tma_load_3d(kt + 32768, &vmap, 0, h, j * 128, &kv_full[st]);
+        tc::tma_load_3d(kt + 49152, &vmap, 64, h, j * 128, &kv_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idO = tc::idesc_bf16(128, 128, false, true);
+      const uint32_t q0 = tc::saddr(sm + S::kQ), kv0 = tc::saddr(sm + S::kKV);
+      const uint32_t phi = tc::saddr(sm + S::kPhi), plo = tc::saddr(sm + S::kPlo);
+      auto pv = [&](int i) {
+        tc::bar_wait(p_full, i & 1u);
+        tc::fence_after_sync();
+        const uint32_t vt = kv0 + (i & 1) * S::kStage + 32768;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = tc::smem_desc(vt + kk * 2048, 16384, 1024, tc::kLayoutSw128);
+          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc::mma_bf16(tmem + 256, tc::smem_desc(phi + ao, 16, 1024, tc::kLayoutSw128), bd, idO, (i > 0 || kk > 0));
+          tc::mma_bf16(tmem + 256, tc::smem_desc(plo + ao, 16, 1024, tc::kLayoutSw128), bd, idO, 1u);
+        }
+        tc::mma_commit(o_full);
+        tc::mma_commit(&kv_empty[i & 1]);
+      };
+      tc::bar_wait(q_full, 0);
+      for (int j = 0; j < nt; ++j) {
+        const int st = j & 1;
+        tc::bar_wait(&kv_full[st], (j >> 1) & 1u);
+        tc::bar_wait(&s_empty[st], ((j >> 1) & 1u) ^ 1u);
+        tc::fence_after_sync();
+        const uint32_t kt = kv0 + st * S::kStage;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc::mma_bf16(tmem + st * 128, tc::smem_desc(q0 + o, 16, 1024, tc::kLayoutSw128),
+                       tc::smem_desc(kt + o, 16, 1024, tc::kLayoutSw128), idS, kk > 0);
+        }
+        tc::mma_commit(&s_full[st]);
+        if (j > 0) pv(j - 1);
+      }
+      pv(nt - 1);
+    }
+  } else {
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;  // query row within the tile = TMEM lane
+    const int row = qt * 128 + r;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    float m_run = -INFINITY, l_run = 0.f;
+    float s[128];
+    for (int j = 0; j < nt; ++j) {
+      const int sb = j & 1;
+      tc::bar_wait(&s_full[sb], (j >> 1) & 1u);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tl + sb * 128 + c * 32, s + c * 32);
+      tc::tmem_wait_ld();
+      tc::fence_before_sync();
+      tc::bar_arrive(&s_empty[sb]);
+      float mt = -INFINITY;
+      const int lim = (j == qt) ? r : 127;  // causal: key j*128+c <= row
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        s[c] = (c <= lim) ? s[c] * scale_log2 : -INFINITY;
+        mt = fmaxf(mt, s[c]);
+      }
+      // lazy rescale: move the reference max only when the tile exceeds it by > 2^8
+      float corr = 1.f;
+      bool resc = false;
+      if (mt > m_run + 8.f) {
+        corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
+        resc = j > 0;
+        m_run = mt;
+        l_run *= corr;
+      }
+      float ls = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; ++c) {
+        s[c] = exp2f(s[c] - m_run);
+        ls += s[c];
+      }
+      l_run += ls;
+      if (j > 0) {
+        tc::bar_wait(o_full, (j - 1) & 1u);  // PV(j-1) done: O stable, P buffers free
+        tc::fence_after_sync();
+      }
+      if (__any_sync(0xffffffffu, resc)) {
+        const float f = resc ? corr : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float o[32];
+          tc::tmem_ld32(tl + 256 + c * 32, o);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= f;
+          tc::tmem_st32(tl + 256 + c * 32, o);
+        }
+        tc::tmem_wait_st();
+      }
+      // P row r: 16 x 16 B chunks, chunk c -> half c/8, swizzled position
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        uint32_t hi[4], lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float a = s[c * 8 + 2 * i], b = s[c * 8 + 2 * i + 1];
+          hi[i] = tc::pack_bf16(a, b);
+          lo[i] = tc::pack_bf16(a - __uint_as_float(hi[i] << 16), b - __uint_as_float(hi[i] & 0xFFFF0000u));
+        }
+        const uint32_t off = (c >> 3) * 16384 + tc::sw128_off(r, c & 7);
+        *reinterpret_cast<uint4*>(sm + S::kPhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
+        *reinterpret_cast<uint4*>(sm + S::kPlo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+      }
+      tc::fence_async_smem();
+      tc::fence_before_sync();
+      tc::bar_arrive(p_full);
+    }
+    tc::bar_wait(o_full, (nt - 1) & 1u);
+    tc::fence_after_sync();
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    const long long obase = (static_cast<long long>(row) * Hq + hq) * 128;
+    __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + obase;
+    float* dstf = static_cast<float*>(out) + obase;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      float o[32];
+      tc::tmem_ld32(tl + 256 + c * 32, o);
+      tc::tmem_wait_ld();
+      if (row < tokens && out_f32) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          *reinterpret_cast<float4*>(dstf + c * 32 + i * 4) =
+              make_float4(o[4 * i] * inv, o[4 * i + 1] * inv, o[4 * i + 2] * inv, o[4 * i + 3] * inv);
+      } else if (row < tokens) {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          uint4 v;
+          v.x = tc::pack_bf16(o[8 * i + 0] * inv, o[8 * i + 1] * inv);
+          v.y = tc::pack_bf16(o[8 * i + 2] * inv, o[8 * i + 3] * inv);
+          v.z = tc::pack_bf16(o[8 * i + 4] * inv, o[8 * i + 5] * inv);
+          v.w = tc::pack_bf16(o[8 * i + 6] * inv, o[8 * i + 7] * inv);
+          *reinterpret_cast<uint4*>(dst + c * 32 + i * 8) = v;
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_free<512>(tmem);
+}
+
+}  // namespace lkv

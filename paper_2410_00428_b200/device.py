@@ -90,6 +90,13 @@ class Device:
         s = None if stream is None else C.c_void_p(stream.cuda_stream)
         self._lib.call("lkv_prefill_layer", self.handle, request_id, layer, _ptr(k), _ptr(v), tokens, s)
 
+    def prefill_attention(self, q, k, v, out, tokens: int, scale: float, out_dtype: int = DTYPE_BF16, stream=None):
+        """Causal GQA attention of one prefill layer on the tensor cores:
+        q/out [tokens][q_heads_local][d], k/v [tokens][kv_heads_local][d] (bf16; out bf16 or fp32)."""
+        s = None if stream is None else C.c_void_p(stream.cuda_stream)
+        self._lib.call("lkv_prefill_attention", self.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), tokens, scale,
+                       out_dtype, s)
+
     def prefill_offload_done(self, request_id: int) -> bool:
         out = C.c_int32()
         self._lib.call("lkv_device_prefill_offload_done", self.handle, request_id, C.byref(out))
