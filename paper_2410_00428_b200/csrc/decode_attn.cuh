@@ -18,8 +18,8 @@
 //    a value-splitting butterfly (8 shuffles for 8 rows); online softmax in
 //    the log2 domain; P.V in fp32. G query heads of a GQA group share every
 //    K/V byte.
-//  * Each unit writes an unnormalised partial (m, l, o) — merged per
-//    (sequence, query head) by decode_merge_v2_kernel.
+//  * Each unit writes an unnormalised partial (m, l, o), merged per
+//    (sequence, query head) by decode_merge_v3_kernel (one warp each).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -98,6 +98,72 @@ __device__ __forceinline__ void cvt8(const uint4& u, float* f) {
 constexpr int kSubTok = 16;                   // tokens per sub-tile
 constexpr int kHeadDim = 128;
 constexpr int kSubBytes = kSubTok * kHeadDim * 2;  // 4 KiB of K (or V) per head
+
+// Split merge of one (sequence, KV head): folds every chunk's unnormalised
+// partial into the output rows of the group's query heads,
+//   out[m][hq][d] = sum_c 2^(m_c - M) o_c / sum_c 2^(m_c - M) l_c.
+// NT cooperating threads, thread t owns dims [t*128/NT, (t+1)*128/NT), query
+// heads g0, g0+gstep, ...; lanes stride over chunks for the maxima and the
+// weights, and the o rows stream with 8 loads in flight per thread.
+// (Fusing this into the attention kernels' last unit was measured slower:
+// the per-unit fence + election cost more than the extra launch.)
+template <int NT>
+__device__ __forceinline__ void merge_kv_head(const float* __restrict__ part_o, const float* __restrict__ part_ml,
+                                              int chunk0, int nch, int h, int Hl, int G, long long out_row0,
+                                              void* __restrict__ out, int out_f32, int t, int g0 = 0,
+                                              int gstep = 1) {
+  constexpr int DPT = kHeadDim / NT;
+  const int lane = t & 31;
+  const long long cstride = static_cast<long long>(Hl) * G;  // partial units between chunks
+  for (int g = g0; g < G; g += gstep) {
+    const long long pu0 = (static_cast<long long>(chunk0) * Hl + h) * G + g;
+    // per-chunk maxima: lanes stride over the chunks (one round trip for <= 32)
+    float M = -INFINITY;
+    for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(part_ml + (pu0 + c * cstride) * 2));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+    float o[DPT], L = 0.f;
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) o[i] = 0.f;
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+      const int c = c0 + lane;
+      float f = 0.f;
+      if (c < nch) {
+        const float2 ml = __ldcg(reinterpret_cast<const float2*>(part_ml + (pu0 + c * cstride) * 2));
+        f = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
+        L = fmaf(f, ml.y, L);
+      }
+      const int n = min(32, nch - c0);
+      // weighted sum of the chunks' o rows, 8 loads in flight per thread
+#pragma unroll 8
+      for (int k = 0; k < n; ++k) {
+        const float fk = __shfl_sync(0xffffffffu, f, k);
+        const float* src = part_o + (pu0 + (c0 + k) * cstride) * kHeadDim + t * DPT;
+        if constexpr (DPT == 4) {
+          const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
+          o[0] = fmaf(fk, v.x, o[0]);
+          o[1] = fmaf(fk, v.y, o[1]);
+          o[2] = fmaf(fk, v.z, o[2]);
+          o[3] = fmaf(fk, v.w, o[3]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < DPT; ++i) o[i] = fmaf(fk, __ldcg(src + i), o[i]);
+        }
+      }
+    }
+#pragma unroll
+    for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
+    const float inv = L > 0.f ? 1.f / L : 0.f;
+    const long long idx = (out_row0 + g) * kHeadDim + t * DPT;
+#pragma unroll
+    for (int i = 0; i < DPT; ++i) {
+      if (out_f32)
+        static_cast<float*>(out)[idx + i] = o[i] * inv;
+      else
+        static_cast<__nv_bfloat16*>(out)[idx + i] = __float2bfloat16_rn(o[i] * inv);
+    }
+  }
+}
 
 template <int G, int BS, int W, int S>
 struct AttnV2 {
@@ -288,8 +354,22 @@ __global__ void __launch_bounds__(W * 32, 1) decode_attn_v2_kernel(
   }
 }
 
-// out[m][hq][d] = sum_c 2^(m_c - M) o_c / sum_c 2^(m_c - M) l_c over the
-// member's chunks (unit = chunk * Hl + kv head).
+// One warp per (member, query head); 4 warps per CTA.
+__global__ void __launch_bounds__(128) decode_merge_v3_kernel(const float* __restrict__ part_o,
+                                                              const float* __restrict__ part_ml,
+                                                              const AttnSeq* __restrict__ seqs, int n, int Hl, int G,
+                                                              void* __restrict__ out, int out_f32) {
+  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int Hq = Hl * G;
+  if (w >= n * Hq) return;
+  const int m = w / Hq, hq = w % Hq, h = hq / G, g = hq % G;
+  const AttnSeq sd = seqs[m];
+  merge_kv_head<32>(part_o, part_ml, sd.chunk0, sd.nchunk, h, Hl, G, (static_cast<long long>(m) * Hl + h) * G, out,
+                    out_f32, threadIdx.x & 31, g, G);
+}
+
+// Previous merge (one CTA per (member, query head), thread = dim).
+// out[m][hq][d] over the member's chunks (unit = chunk * Hl + kv head).
 __global__ void decode_merge_v2_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
                                        const AttnSeq* __restrict__ seqs, int Hl, int G, void* __restrict__ out,
                                        int out_f32) {

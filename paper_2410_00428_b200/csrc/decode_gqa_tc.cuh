@@ -26,7 +26,7 @@
 //            softmax correction (no TMEM read-modify-write hazard).
 // Work unit = (chunk of blocks of one sequence, one KV head), exactly as the
 // CUDA-core kernel (decode_attn.cuh), and the partial (m, l, o) per query head
-// is merged by decode_merge_v2_kernel.
+// is merged by decode_merge_v3_kernel.
 #pragma once
 
 #include <cuda_bf16.h>

@@ -133,6 +133,7 @@ struct lkv_device final : layersim::KvObserver {
   // bulk copies (decode_attn.cuh), 3 = tcgen05 GQA tile (decode_gqa_tc.cuh).
   // LKV_DECODE_KERNEL overrides the per-group-size default.
   int kernel_version = 2;
+  int merge_version = 3;           // LKV_MERGE=2: one CTA per (member, query head), thread = dim
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
@@ -236,6 +237,7 @@ struct lkv_device final : layersim::KvObserver {
       const int v = std::atoi(kv);
       kernel_version = (v == 1 || v == 3) ? v : 2;
     }
+    if (const char* mv = std::getenv("LKV_MERGE")) merge_version = std::atoi(mv) == 2 ? 2 : 3;
     {
       const unsigned long long rows = static_cast<unsigned long long>(std::max<long long>(frames, 1)) * 2 * Hl * bs;
       if (rows > 0x7FFFFFFFull) throw CapacityError("pool + arena rows exceed the TMA coordinate range");
@@ -720,7 +722,7 @@ struct lkv_device final : layersim::KvObserver {
 
   // ---- v3: tcgen05 GQA tile (decode_gqa_tc.cuh) -------------------------------
   template <int GG, int BB>
-  void launch_tc(int l, const void* q, float sl2) {
+  void launch_tc(int l, const void* q, float sl2, void* out, int f32) {
     constexpr int NS = 3;
     using K = GqaTc<GG, BB, NS>;
     auto fn = decode_gqa_tc_kernel<GG, BB, NS>;
@@ -737,14 +739,14 @@ struct lkv_device final : layersim::KvObserver {
   }
 
   template <int GG>
-  void launch_tc_bs(int l, const void* q, float sl2) {
-    if (bs == 16) launch_tc<GG, 16>(l, q, sl2);
-    else if (bs == 32) launch_tc<GG, 32>(l, q, sl2);
-    else launch_tc<GG, 64>(l, q, sl2);
+  void launch_tc_bs(int l, const void* q, float sl2, void* out, int f32) {
+    if (bs == 16) launch_tc<GG, 16>(l, q, sl2, out, f32);
+    else if (bs == 32) launch_tc<GG, 32>(l, q, sl2, out, f32);
+    else launch_tc<GG, 64>(l, q, sl2, out, f32);
   }
 
   template <int GG, int BB, int W, int S>
-  void launch_v2_cfg(int l, const void* q, float sl2) {
+  void launch_v2_cfg(int l, const void* q, float sl2, void* out, int f32) {
     using K = AttnV2<GG, BB, W, S>;
     auto fn = decode_attn_v2_kernel<GG, BB, W, S>;
     static bool attr_set = false;  // per instantiation
@@ -760,18 +762,18 @@ struct lkv_device final : layersim::KvObserver {
   }
 
   template <int GG, int BB>
-  void launch_v2(int l, const void* q, float sl2) {
+  void launch_v2(int l, const void* q, float sl2, void* out, int f32) {
     if constexpr (GG == 1)
-      launch_v2_cfg<GG, BB, 12, 2>(l, q, sl2);
+      launch_v2_cfg<GG, BB, 12, 2>(l, q, sl2, out, f32);
     else
-      launch_v2_cfg<GG, BB, 8, 3>(l, q, sl2);
+      launch_v2_cfg<GG, BB, 8, 3>(l, q, sl2, out, f32);
   }
 
   template <int GG>
-  void launch_v2_bs(int l, const void* q, float sl2) {
-    if (bs == 16) launch_v2<GG, 16>(l, q, sl2);
-    else if (bs == 32) launch_v2<GG, 32>(l, q, sl2);
-    else launch_v2<GG, 64>(l, q, sl2);
+  void launch_v2_bs(int l, const void* q, float sl2, void* out, int f32) {
+    if (bs == 16) launch_v2<GG, 16>(l, q, sl2, out, f32);
+    else if (bs == 32) launch_v2<GG, 32>(l, q, sl2, out, f32);
+    else launch_v2<GG, 64>(l, q, sl2, out, f32);
   }
 
   template <int GG, int BB>
@@ -801,22 +803,26 @@ struct lkv_device final : layersim::KvObserver {
       const float sl2 = scale * 1.4426950408889634f;
       if (n_chunks > 0 && kernel_version == 3) {
         switch (G) {
-          case 1: launch_tc_bs<1>(l, q, sl2); break;
-          case 2: launch_tc_bs<2>(l, q, sl2); break;
-          case 4: launch_tc_bs<4>(l, q, sl2); break;
-          default: launch_tc_bs<8>(l, q, sl2); break;
+          case 1: launch_tc_bs<1>(l, q, sl2, out, f32); break;
+          case 2: launch_tc_bs<2>(l, q, sl2, out, f32); break;
+          case 4: launch_tc_bs<4>(l, q, sl2, out, f32); break;
+          default: launch_tc_bs<8>(l, q, sl2, out, f32); break;
         }
         LKV_CUDA(cudaGetLastError());
       } else if (n_chunks > 0) {
         switch (G) {
-          case 1: launch_v2_bs<1>(l, q, sl2); break;
-          case 2: launch_v2_bs<2>(l, q, sl2); break;
-          case 4: launch_v2_bs<4>(l, q, sl2); break;
-          default: launch_v2_bs<8>(l, q, sl2); break;
+          case 1: launch_v2_bs<1>(l, q, sl2, out, f32); break;
+          case 2: launch_v2_bs<2>(l, q, sl2, out, f32); break;
+          case 4: launch_v2_bs<4>(l, q, sl2, out, f32); break;
+          default: launch_v2_bs<8>(l, q, sl2, out, f32); break;
         }
         LKV_CUDA(cudaGetLastError());
       }
-      decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
+      // merge (members without KV get zero rows: no chunks, L = 0)
+      if (merge_version == 2)
+        decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
+      else
+        decode_merge_v3_kernel<<<(n * Hql + 3) / 4, 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, n, Hl, G, out, f32);
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;
       dstats.kernel_launches += n_chunks > 0 ? 2 : 1;
