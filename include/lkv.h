@@ -293,6 +293,23 @@ LKV_API int lkv_decode_layer(lkv_device* dev, int32_t layer, const void* q, void
                              int32_t out_dtype);
 LKV_API int lkv_decode_end(lkv_device* dev);
 
+/* Serving decode with KV write-back. Like lkv_decode_begin,
+ * but the iteration also appends each member's new token at position
+ * cached_tokens (the block append_decode_block provided, engine.cpp:408-409)
+ * and attention covers cached_tokens + 1 keys. The fetch booked is still
+ * plan_decode_fetch's (cached tokens only). Per layer call
+ * lkv_decode_append_layer before lkv_decode_layer; note_token afterwards as
+ * in the reference (engine.cpp:151). */
+LKV_API int lkv_decode_begin_append(lkv_device* dev, const int64_t* request_ids, int32_t n);
+/* k_new/v_new [n][kv_heads_local][head_dim] bf16 on the device, members in
+ * decode_begin order. The token row goes wherever its slot lives: the GPU
+ * slot, or the pinned host frame of a CPU slot plus its prefetched arena copy
+ * (read by this step's attention); an entry whose offload is in flight gets
+ * its GPU slot and its destination frame, ordered after the in-flight D2H.
+ * The reference allocates these slots (kv_manager.cpp:313-344) but never
+ * schedules the bytes. */
+LKV_API int lkv_decode_append_layer(lkv_device* dev, int32_t layer, const void* k_new, const void* v_new);
+
 typedef struct lkv_decode_stats {
   int64_t h2d_bytes_physical;    /* whole slots copied */
   int64_t h2d_bytes_algorithmic; /* token-exact, = sum of plan_decode_fetch bytes */

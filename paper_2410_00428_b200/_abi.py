@@ -157,6 +157,8 @@ _PROTOS = {
     "lkv_device_prefill_offload_done": [vp, i64, P(i32)],
     "lkv_decode_begin": [vp, P(i64), i32],
     "lkv_decode_layer": [vp, i32, vp, vp, f32, i32],
+    "lkv_decode_begin_append": [vp, P(i64), i32],
+    "lkv_decode_append_layer": [vp, i32, vp, vp],
     "lkv_decode_end": [vp],
     "lkv_device_set_timing": [vp, i32],
     "lkv_decode_last_stats": [vp, P(DecodeStats)],
@@ -169,6 +171,7 @@ _RET = {"lkv_last_error": C.c_char_p, "lkv_version": C.c_char_p}
 
 DEVICE_SYMBOLS = [n for n in _PROTOS if n.startswith(("lkv_device", "lkv_prefill_layer", "lkv_prefill_attention", "lkv_decode_begin",
                                                      "lkv_decode_layer", "lkv_decode_end", "lkv_decode_last",
+                                                     "lkv_decode_append",
                                                      "lkv_offload_last", "lkv_fill", "lkv_verify"))]
 ALL_SYMBOLS = list(_PROTOS) + list(_RET)
 

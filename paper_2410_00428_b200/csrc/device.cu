@@ -166,7 +166,10 @@ struct lkv_device final : layersim::KvObserver {
   struct Member {
     long long id;
     int row, kv_len, nblk, blk_off;
+    int fetch_len;  // cached tokens at decode_begin: what plan_decode_fetch books
   };
+  bool append_mode = false;        // lkv_decode_begin_append: the step appends one token per member
+  std::vector<char> appended;      // [L] append issued for the layer this iteration
   std::vector<Member> members;
   int total_blocks = 0, max_nblk = 0;
   bool in_iteration = false;
@@ -218,12 +221,12 @@ struct lkv_device final : layersim::KvObserver {
     const long long frames = cfg.gpu_slots + cfg.arena_slots * cfg.pipeline_depth;
     if (frames > 0x7FFFFFFFll) throw CapacityError("pool + arena frames exceed int32 indexing");
     LKV_CUDA(cudaMalloc(&dbuf, std::max<long long>(frames, 1) * sb));
+
     if (cfg.host_slots > 0)
       LKV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool), cfg.host_slots * sb,
                              cudaHostAllocMapped | cudaHostAllocPortable));
     const long long tbl = static_cast<long long>(cfg.max_requests) * L * cfg.max_blocks;
     LKV_CUDA(cudaMalloc(&d_table, tbl * sizeof(int)));
-    LKV_CUDA(cudaMemset(d_table, 0, tbl * sizeof(int)));
     LKV_CUDA(cudaMalloc(&d_snap, std::max<long long>(1, static_cast<long long>(L) * cfg.arena_slots) *
                                      sizeof(int)));
     LKV_CUDA(cudaMalloc(&d_seqs, cfg.max_batch * sizeof(SeqDesc)));
@@ -255,6 +258,12 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking));
     LKV_CUDA(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
     LKV_CUDA(cudaStreamCreateWithFlags(&h2d, cudaStreamNonBlocking));
+    // Attention reads whole blocks and masks the tail; never let a tail be an
+    // uninitialised NaN pattern (0 * NaN poisons P.V). Ordered on the compute
+    // stream (a legacy-stream memset would race the non-blocking streams).
+    LKV_CUDA(cudaMemsetAsync(dbuf, 0, std::max<long long>(frames, 1) * sb, cs));
+    LKV_CUDA(cudaMemsetAsync(d_table, 0, tbl * sizeof(int), cs));
+    LKV_CUDA(cudaStreamSynchronize(cs));
     seg_ready.resize(cfg.staging_chunks);
     seg_free.resize(cfg.staging_chunks);
     seg_used.assign(cfg.staging_chunks, 0);
@@ -601,12 +610,13 @@ struct lkv_device final : layersim::KvObserver {
       dst.clear();
       long long tok = 0;
       for (int b = 0; b < m.nblk; ++b) {
+        if (static_cast<long long>(b) * bs >= m.fetch_len) break;  // the appended token's fresh block
         const auto& e = r.blocks[b].layers[l];
         if (e.loc != Loc::Cpu) continue;
         check_slot(e);
         src.push_back(e.slot);
         dst.push_back(arena0 + m.blk_off + b);
-        tok += std::clamp<long long>(m.kv_len - static_cast<long long>(b) * bs, 0, bs);
+        tok += std::clamp<long long>(m.fetch_len - static_cast<long long>(b) * bs, 0, bs);
       }
       if (src.empty()) continue;
       dstats.h2d_copies += emit_copies(dbuf, dst.data(), host_pool, src.data(),
@@ -618,8 +628,10 @@ struct lkv_device final : layersim::KvObserver {
     if (timing) LKV_CUDA(cudaEventRecord(t_h2d1, h2d));
   }
 
-  void decode_begin(const int64_t* ids, int n) {
+  void decode_begin(const int64_t* ids, int n, bool append = false) {
     if (in_iteration) throw layersim::SimulationError("decode_begin: iteration already open");
+    append_mode = append;
+    appended.assign(L, 0);
     if (n < 0 || n > cfg.max_batch) throw CapacityError("decode batch exceeds max_batch");
     flush();
     members.clear();
@@ -633,8 +645,12 @@ struct lkv_device final : layersim::KvObserver {
       Member m;
       m.id = ids[i];
       m.row = row_for(ids[i]);
-      m.kv_len = static_cast<int>(r.cached_tokens);
-      m.nblk = static_cast<int>(std::min<long long>((r.cached_tokens + bs - 1) / bs, static_cast<long long>(r.blocks.size())));
+      m.fetch_len = static_cast<int>(r.cached_tokens);
+      m.kv_len = m.fetch_len + (append ? 1 : 0);
+      if (append && static_cast<long long>(r.blocks.size()) * bs < m.kv_len)
+        throw layersim::SimulationError("decode append: request " + std::to_string(ids[i]) +
+                                        " has no block for its next token (append_decode_block first)");
+      m.nblk = static_cast<int>(std::min<long long>((m.kv_len + bs - 1) / bs, static_cast<long long>(r.blocks.size())));
       m.blk_off = total_blocks;
       total_blocks += m.nblk;
       max_nblk = std::max(max_nblk, m.nblk);
@@ -792,9 +808,68 @@ struct lkv_device final : layersim::KvObserver {
     else launch_attn<GG, 64>(l, n_split, bps, q, out, f32, sl2);
   }
 
+  // f2: write each member's new token (position fetch_len) of layer l wherever
+  // its slot lives. Destinations are resolved on the host from the manager's
+  // table: the GPU slot, or the CPU slot's pinned frame plus its arena copy
+  // (this step's attention reads the arena), or — offload in flight — the GPU
+  // slot and the destination frame, after the D2H already carrying the block.
+  void decode_append_layer(int l, const void* k, const void* v) {
+    if (!in_iteration || !append_mode)
+      throw layersim::SimulationError("decode_append_layer outside decode_begin_append/end");
+    check_layer(l);
+    if (appended[l]) throw layersim::SimulationError("decode_append_layer: layer appended twice");
+    const int st = l % cfg.pipeline_depth;
+    const long long arena0 = cfg.gpu_slots + static_cast<long long>(st) * cfg.arena_slots;
+    const int n = static_cast<int>(members.size());
+    auto* dd = reinterpret_cast<AppendDesc*>(ring.reserve(std::max(n, 1) * sizeof(AppendDesc)));
+    bool inflight = false;
+    for (int i = 0; i < n; ++i) {
+      const Member& m = members[i];
+      const RequestKv& r = kv->request(m.id);
+      const int b = m.fetch_len / bs;
+      const auto& e = r.blocks[b].layers[l];
+      AppendDesc a{};
+      a.tok = m.fetch_len % bs;
+      if (e.loc == Loc::Gpu) {
+        check_slot(e);
+        a.dst[0] = dbuf + static_cast<long long>(e.slot) * sb;
+        if (e.offload_in_flight) {
+          if (static_cast<long long>(e.dest_slot) >= cfg.host_slots) throw CapacityError("append: dest frame");
+          a.dst[1] = host_pool + static_cast<long long>(e.dest_slot) * sb;
+          inflight = true;
+        }
+      } else if (e.loc == Loc::Cpu) {
+        check_slot(e);
+        a.dst[0] = host_pool + static_cast<long long>(e.slot) * sb;
+        a.dst[1] = dbuf + (arena0 + m.blk_off + b) * sb;
+      } else {
+        throw layersim::SimulationError("decode append: token slot has no location");
+      }
+      dd[i] = a;
+    }
+    LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));  // the arena copy lands first
+    if (inflight) {
+      cudaEvent_t ev;
+      ev_create(&ev);
+      LKV_CUDA(cudaEventRecord(ev, d2h));
+      LKV_CUDA(cudaStreamWaitEvent(cs, ev, 0));
+      cudaEventDestroy(ev);
+    }
+    if (n > 0) {
+      append_kv_kernel<<<n, 256, 0, cs>>>(dd, static_cast<const __nv_bfloat16*>(k),
+                                          static_cast<const __nv_bfloat16*>(v), Hl, bs, D);
+      LKV_CUDA(cudaGetLastError());
+      dstats.kernel_launches += 1;
+    }
+    ring.commit(cs);
+    appended[l] = 1;
+  }
+
   void decode_layer(int l, const void* q, void* out, float scale, int f32) {
     if (!in_iteration) throw layersim::SimulationError("decode_layer outside decode_begin/end");
     check_layer(l);
+    if (append_mode && !appended[l])
+      throw layersim::SimulationError("decode_layer: append mode needs decode_append_layer first");
     const int st = l % cfg.pipeline_depth;
     LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));
     const int n = static_cast<int>(members.size());
@@ -1009,6 +1084,20 @@ int lkv_decode_begin(lkv_device* d, const int64_t* ids, int32_t n) {
   LKV_REQUIRE(d && d->kv && (ids || n == 0));
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
   d->decode_begin(ids, n);
+  LKV_CATCH
+}
+
+int lkv_decode_begin_append(lkv_device* d, const int64_t* ids, int32_t n) {
+  LKV_REQUIRE(d && d->kv && (ids || n == 0));
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->decode_begin(ids, n, true);
+  LKV_CATCH
+}
+
+int lkv_decode_append_layer(lkv_device* d, int32_t layer, const void* k_new, const void* v_new) {
+  LKV_REQUIRE(d && d->kv && k_new && v_new);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->decode_append_layer(layer, k_new, v_new);
   LKV_CATCH
 }
 

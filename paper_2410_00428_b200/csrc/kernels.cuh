@@ -126,6 +126,33 @@ __global__ void gather_slots_kernel(const char* __restrict__ pool, const unsigne
 // a physical frame of the unified [pool | arena] buffer. GPU entries keep
 // their slot id; CPU entries (encoded ~cpu_slot) point at the arena frame the
 // prefetch writes: arena0 + member_base + b.
+// Decode-time append (f2): one member's new token of one layer. Up to two
+// destination frames (slot base addresses; host frames are mapped pinned
+// memory written over the link), token row `tok` of every head's K and V.
+struct AppendDesc {
+  char* dst[2];
+  int tok;
+  int pad;
+};
+
+__global__ void append_kv_kernel(const AppendDesc* __restrict__ desc, const __nv_bfloat16* __restrict__ k,
+                                 const __nv_bfloat16* __restrict__ v, int Hl, int bs, int D) {
+  const AppendDesc a = desc[blockIdx.x];
+  const int vec_per_row = D / 8;
+  const int total = 2 * Hl * vec_per_row;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int c = i % vec_per_row;
+    const int h = (i / vec_per_row) % Hl;
+    const int kvsel = i / (vec_per_row * Hl);
+    const __nv_bfloat16* src = (kvsel ? v : k) + (static_cast<long long>(blockIdx.x) * Hl + h) * D + c * 8;
+    const uint4 val = *reinterpret_cast<const uint4*>(src);
+    const long long off = ((static_cast<long long>(kvsel) * Hl + h) * bs + a.tok) * D * 2 + c * 16;
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+      if (a.dst[j]) *reinterpret_cast<uint4*>(a.dst[j] + off) = val;
+  }
+}
+
 struct SeqDesc {
   int row_offset;   // table offset of (row, layer 0, block 0)
   int kv_len;       // tokens attended

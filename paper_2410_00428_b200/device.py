@@ -112,6 +112,14 @@ class Device:
         arr = (C.c_int64 * max(1, len(request_ids)))(*request_ids)
         self._lib.call("lkv_decode_begin", self.handle, arr, len(request_ids))
 
+    def decode_begin_append(self, request_ids):
+        """Serving decode: this iteration appends one token per member (f2)."""
+        arr = (C.c_int64 * max(1, len(request_ids)))(*request_ids)
+        self._lib.call("lkv_decode_begin_append", self.handle, arr, len(request_ids))
+
+    def decode_append_layer(self, layer: int, k_new, v_new):
+        self._lib.call("lkv_decode_append_layer", self.handle, layer, _ptr(k_new), _ptr(v_new))
+
     def decode_layer(self, layer: int, q, out, scale: float, out_dtype: int = DTYPE_BF16):
         self._lib.call("lkv_decode_layer", self.handle, layer, _ptr(q), _ptr(out), scale, out_dtype)
 
