@@ -60,6 +60,7 @@ def parse():
     p.add_argument("--depth", type=int, default=2, help="prefetch pipeline depth (layers in flight)")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
+    p.add_argument("--no-rows", action="store_true", help="skip the tensor-core / overlap rows beside the headline")
     return p.parse_args()
 
 
@@ -70,6 +71,15 @@ def peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def tensor_peak():
+    """Dense bf16 TFLOP/s: measured burst (MEASURED_PEAKS.json), else the profiling guide's fallback."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["bf16_tflops"])
+    except Exception:
+        return 2250.0
 
 
 # ------------------------------------------------------------------ clocks
@@ -246,6 +256,120 @@ def workload_config(args):
             "parallelism": f"kv-head tp{args.gpus}", "pipeline_depth": args.depth}
 
 
+# ------------------------------------------------------------------ §8 rows beside the headline
+def ev_ms(torch, stream, fn, iters=1):
+    """CUDA-event time of fn() on `stream` (synchronised on both sides)."""
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        fn()
+    e1.record(stream)
+    e1.synchronize()
+    return e0.elapsed_time(e1) / iters
+
+
+def prefill_rows(torch, dev_t, link, tf_peak):
+    """a20 + a14 on config 2's 16k LayerKV request (7B, x=0: every layer
+    offloaded, reference min_retained_layers): per layer the causal prefill
+    attention on the tcgen05 kernel, then lkv_prefill_layer packs the layer's
+    K/V and streams it to the CPU slots' pinned frames on the D2H engine while
+    the next layer's attention runs. Reports the attention kernel against the
+    measured bf16 peak and how much of the offload the compute hides."""
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+    model = ls.llama2_7b()
+    L, bs, d, T = model.n_layers, 16, model.d_head, 16384
+    nblk = T // bs
+    kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model)
+    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=64, host_slots=nblk * L + 64,
+                                             arena_slots=64, max_requests=4, max_blocks=nblk + 8, max_batch=2))
+    hq, hl = dev.q_heads_local, dev.kv_heads_local
+    cs = dev.torch_stream("compute")
+    g = torch.Generator(device=dev_t).manual_seed(3)
+    q = (torch.rand((T, hq, d), device=dev_t, generator=g) * 2 - 1).to(torch.bfloat16)
+    k = torch.empty((T, hl, d), dtype=torch.bfloat16, device=dev_t)
+    v = torch.empty_like(k)
+    out = torch.empty_like(q)
+    scale = 1.0 / math.sqrt(d)
+    dev.fill_kv(k, v, T, 0, 0, SEED, stream=cs)
+    attn = lambda: dev.prefill_attention(q, k, v, out, T, scale, DTYPE_BF16, stream=cs)  # noqa: E731
+    attn()
+    attn_ms = min(ev_ms(torch, cs, attn) for _ in range(3))
+    flops = 4.0 * d * hq * T * (T + 1) / 2
+    # whole prompt: per layer attention + offload of the layer (compute-only run first)
+    compute_ms = ev_ms(torch, cs, lambda: [attn() for _ in range(L)])
+    assert kv.allocate_prefill(0, T, 0)
+
+    def prefill_with_offload():
+        for layer in range(L):
+            attn()
+            dev.prefill_layer(0, layer, k, v, T, stream=cs)
+        dev.synchronize()
+    t0 = time.perf_counter()
+    prefill_with_offload()
+    with_ms = (time.perf_counter() - t0) * 1e3
+    ost = dev.offload_stats(reset=True)
+    bytes_off = ost.d2h_bytes_algorithmic
+    link_ms = bytes_off / (link["d2h"] * 1e9) * 1e3
+    exposed = max(0.0, with_ms - compute_ms)
+    # simulated TTFT of the same prefill (reference cost model, B200-like hardware spec)
+    hw = ls.HardwareSpec(tf_peak * 1e12, 6.55e12, link["d2h"] * 1e9, True, 1, 180e9, 0.9)
+    sim = ls.prefill_time(model, hw, ls.CostParams(), T)
+    dev.close()
+    return {
+        "a20_prefill_attention": {
+            "kernel": "prefill_attn_kernel (tcgen05, causal GQA)", "shape": f"7B MHA 32 heads, {T} tokens, 1 layer",
+            "ms": attn_ms, "tflops": flops / attn_ms / 1e9, "peak_tflops": tf_peak,
+            "frac": flops / attn_ms / 1e9 / tf_peak, "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)"},
+        "a14_prefill_offload_overlap": {
+            "workload": f"1 request x {T} tokens, 7B, x=0 (all {L} layers offloaded): attention + pack + D2H per layer",
+            "compute_only_ms": compute_ms, "with_offload_ms": with_ms, "exposed_offload_ms": exposed,
+            "offload_bytes": bytes_off, "offload_alone_at_link_peak_ms": link_ms,
+            "hidden_frac": max(0.0, 1.0 - exposed / link_ms) if link_ms else None,
+            "offload_gbs_during_prefill": bytes_off / (with_ms / 1e3) / 1e9,
+            "measured_ttft_ms_attention_only": with_ms,
+            "simulated_prefill_s_cost_model": sim},
+    }
+
+
+def gqa_decode_row(torch, dev_t, hbm_peak):
+    """a18 for the GQA configs (3/4): Llama-3-8B shape (Hq 32, Hkv 8), batch
+    16 x 32k context, layers GPU-resident, through the tcgen05 decode tile."""
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+    Lr, bs, B, ctx = 2, 16, 16, 32768
+    model = ls.ModelSpec(Lr, 32, 8, 128, 4096, 8.03e9, 2)
+    nblk = ctx // bs
+    slots = B * nblk * Lr
+    kv = ls.KvManager(ls.BlockPools(slots + 64, 64, bs), model)
+    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=slots + 64, host_slots=64,
+                                             arena_slots=B * nblk + 8, max_requests=B + 1, max_blocks=nblk + 4,
+                                             max_batch=B))
+    ids = list(range(B))
+    for r in ids:
+        assert kv.allocate_prefill(r, ctx, Lr)
+        dev.fill_request(r, ctx, SEED)
+    q = torch.randn((B, dev.q_heads_local, 128), dtype=torch.bfloat16, device=dev_t)
+    out = torch.empty_like(q)
+    dev.set_timing(True)
+    best = None
+    for it in range(4):
+        dev.decode_begin(ids)
+        for layer in range(Lr):
+            dev.decode_layer(layer, q, out, 1 / math.sqrt(128), DTYPE_BF16)
+        dev.decode_end()
+        st = dev.decode_stats()
+        if it >= 1:
+            ms = st.attn_ms / st.attn_launches
+            best = ms if best is None else min(best, ms)
+    byts = B * ctx * ls.kv_bytes_per_token_layer(model)
+    dev.close()
+    return {"kernel": "decode_gqa_tc_kernel (tcgen05, G=4) + merge", "shape": f"8B GQA batch {B} x {ctx}",
+            "ms_per_layer": best, "gbs": byts / (best / 1e3) / 1e9, "peak": hbm_peak,
+            "frac": byts / (best / 1e3) / 1e9 / hbm_peak}
+
+
 # ------------------------------------------------------------------ product arm
 def main():
     args = parse()
@@ -315,7 +439,7 @@ def main():
             if qsrc is not None:
                 with torch.cuda.stream(cs):
                     q[layer].copy_(qsrc[layer], non_blocking=True)
-            dev.decode_layer(layer, q[layer], out[layer], scale, DTYPE_BF16)
+            dev.decode_layer(layer, q[layer], out[layer], scale, DTYPE_BF16, stream=cs)
             if world > 1:
                 with torch.cuda.stream(cs):  # the one collective: all-gather of per-head outputs
                     dist.all_gather_into_tensor(gathered[layer], out[layer].reshape(-1))
@@ -408,7 +532,7 @@ def main():
             "config": workload_config(args),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "decode_attn_kernel (+ split merge)", "peak_kind": peak_kind,
+                         "kernel": "decode_attn_v2_kernel<G=1> + decode_merge_v3_kernel", "peak_kind": peak_kind,
                          "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms},
             "host_link": {"prefetch_gbs_per_gpu": h2d_alg / world / (h2d_ms / 1000) / 1e9 if h2d_ms else None,
                           "prefetch_algorithmic_bytes_per_step": h2d_alg // args.steps * world,
@@ -423,14 +547,20 @@ def main():
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": qbytes + h2d_phys // args.steps,
                     "d2h_bytes_per_step": qbytes},
             "gpu_launches": launches,
+            "rows": None,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
         }
-        print(json.dumps(line), flush=True)
     # pinned tensors used on the device's streams must go before the streams do
     del q_host, out_host, q, out, k, v, gathered
     torch.cuda.synchronize()
     dev.close()
+    if rank == 0:
+        if world == 1 and not args.no_rows:  # §8 rows beside the headline (own devices, after this one is gone)
+            rows = prefill_rows(torch, dev_t, link, tensor_peak())
+            rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak)
+            line["rows"] = rows
+        print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 

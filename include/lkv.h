@@ -259,7 +259,8 @@ LKV_API int lkv_device_synchronize(lkv_device* dev);
  * the pinned host frames of their CPU slots on the D2H stream — the
  * per-layer D2H job of schedule_prefill_span (engine.cpp:35-42). The
  * kernels are ordered after work already on `stream` (NULL = compute
- * stream) via an event. */
+ * stream) via an event, and later work on `stream` waits until k/v have
+ * been read, so the caller may reuse them. */
 LKV_API int lkv_prefill_layer(lkv_device* dev, int64_t request_id, int32_t layer, const void* k,
                       const void* v, int64_t tokens, void* stream);
 /* Causal GQA prefill attention of one layer on the tcgen05 tensor cores —
@@ -286,11 +287,12 @@ LKV_API int lkv_decode_begin(lkv_device* dev, const int64_t* request_ids, int32_
  * for serving, fp32 for parity checks); kv_len of member m = its
  * cached_tokens at decode_begin. Waits for the layer's fetch, runs on the
  * compute stream, then issues the fetch of layer + pipeline_depth. `scale` =
- * softmax scale. */
+ * softmax scale. `stream` (may be NULL) is the caller's stream: q is read
+ * after the work already queued on it, and its later work sees `out`. */
 #define LKV_DTYPE_BF16 0
 #define LKV_DTYPE_F32 1
 LKV_API int lkv_decode_layer(lkv_device* dev, int32_t layer, const void* q, void* out, float scale,
-                             int32_t out_dtype);
+                             int32_t out_dtype, void* stream);
 LKV_API int lkv_decode_end(lkv_device* dev);
 
 /* Serving decode with KV write-back. Like lkv_decode_begin,
@@ -307,8 +309,9 @@ LKV_API int lkv_decode_begin_append(lkv_device* dev, const int64_t* request_ids,
  * (read by this step's attention); an entry whose offload is in flight gets
  * its GPU slot and its destination frame, ordered after the in-flight D2H.
  * The reference allocates these slots (kv_manager.cpp:313-344) but never
- * schedules the bytes. */
-LKV_API int lkv_decode_append_layer(lkv_device* dev, int32_t layer, const void* k_new, const void* v_new);
+ * schedules the bytes. `stream` orders the inputs as in lkv_decode_layer. */
+LKV_API int lkv_decode_append_layer(lkv_device* dev, int32_t layer, const void* k_new, const void* v_new,
+                                    void* stream);
 
 typedef struct lkv_decode_stats {
   int64_t h2d_bytes_physical;    /* whole slots copied */

@@ -156,9 +156,9 @@ _PROTOS = {
     "lkv_device_job_done": [vp, i64, P(i32)],
     "lkv_device_prefill_offload_done": [vp, i64, P(i32)],
     "lkv_decode_begin": [vp, P(i64), i32],
-    "lkv_decode_layer": [vp, i32, vp, vp, f32, i32],
+    "lkv_decode_layer": [vp, i32, vp, vp, f32, i32, vp],
     "lkv_decode_begin_append": [vp, P(i64), i32],
-    "lkv_decode_append_layer": [vp, i32, vp, vp],
+    "lkv_decode_append_layer": [vp, i32, vp, vp, vp],
     "lkv_decode_end": [vp],
     "lkv_device_set_timing": [vp, i32],
     "lkv_decode_last_stats": [vp, P(DecodeStats)],

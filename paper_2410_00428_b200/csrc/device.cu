@@ -290,6 +290,7 @@ struct lkv_device final : layersim::KvObserver {
     ev_create(&t_h2d1, true);
     ev_create(&t_pack0, true);
     ev_create(&t_pack1, true);
+    ev_create(&ev_join);
     for (int r = cfg.max_requests - 1; r >= 0; --r) free_rows.push_back(r);
   }
 
@@ -309,7 +310,7 @@ struct lkv_device final : layersim::KvObserver {
     kill(attn_done);
     kill(t_attn0);
     kill(t_attn1);
-    for (auto e : {t_it0, t_it1, t_h2d0, t_h2d1, t_pack0, t_pack1})
+    for (auto e : {t_it0, t_it1, t_h2d0, t_h2d1, t_pack0, t_pack1, ev_join})
       if (e) cudaEventDestroy(e);
     for (auto& kvp : job_ev) cudaEventDestroy(kvp.second);
     for (auto& kvp : prefill_ev) cudaEventDestroy(kvp.second);
@@ -522,17 +523,26 @@ struct lkv_device final : layersim::KvObserver {
   }
 
   // ---------------------------------------------------------------- prefill
+  // Ordering with a caller's stream: inputs produced on `user` are read on the
+  // compute stream only after join_in; the caller's later work (reusing the
+  // inputs, reading outputs) waits for the compute stream after join_out.
+  cudaEvent_t ev_join = nullptr;
+  void join_in(cudaStream_t user) {
+    if (!user || user == cs) return;
+    LKV_CUDA(cudaEventRecord(ev_join, user));
+    LKV_CUDA(cudaStreamWaitEvent(cs, ev_join, 0));
+  }
+  void join_out(cudaStream_t user) {
+    if (!user || user == cs) return;
+    LKV_CUDA(cudaEventRecord(ev_join, cs));
+    LKV_CUDA(cudaStreamWaitEvent(user, ev_join, 0));
+  }
+
   void prefill_layer(long long id, int l, const void* k, const void* v, long long tokens,
                      cudaStream_t user) {
     check_layer(l);
     flush();
-    if (user && user != cs) {
-      cudaEvent_t ev;
-      ev_create(&ev);
-      LKV_CUDA(cudaEventRecord(ev, user));
-      LKV_CUDA(cudaStreamWaitEvent(cs, ev, 0));
-      cudaEventDestroy(ev);
-    }
+    join_in(user);
     const RequestKv& r = kv->request(id);
     const int row = row_for(id);
     const long long nb = std::min<long long>((tokens + bs - 1) / bs, static_cast<long long>(r.blocks.size()));
@@ -592,6 +602,7 @@ struct lkv_device final : layersim::KvObserver {
       LKV_CUDA(cudaEventRecord(ev, d2h));
     }
     if (timing) LKV_CUDA(cudaEventRecord(t_pack1, cs));
+    join_out(user);  // k/v may be overwritten once the scatter/pack has read them
   }
 
   // ----------------------------------------------------------------- decode
@@ -813,7 +824,7 @@ struct lkv_device final : layersim::KvObserver {
   // table: the GPU slot, or the CPU slot's pinned frame plus its arena copy
   // (this step's attention reads the arena), or — offload in flight — the GPU
   // slot and the destination frame, after the D2H already carrying the block.
-  void decode_append_layer(int l, const void* k, const void* v) {
+  void decode_append_layer(int l, const void* k, const void* v, cudaStream_t user) {
     if (!in_iteration || !append_mode)
       throw layersim::SimulationError("decode_append_layer outside decode_begin_append/end");
     check_layer(l);
@@ -847,6 +858,7 @@ struct lkv_device final : layersim::KvObserver {
       }
       dd[i] = a;
     }
+    join_in(user);
     LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));  // the arena copy lands first
     if (inflight) {
       cudaEvent_t ev;
@@ -863,14 +875,16 @@ struct lkv_device final : layersim::KvObserver {
     }
     ring.commit(cs);
     appended[l] = 1;
+    join_out(user);
   }
 
-  void decode_layer(int l, const void* q, void* out, float scale, int f32) {
+  void decode_layer(int l, const void* q, void* out, float scale, int f32, cudaStream_t user) {
     if (!in_iteration) throw layersim::SimulationError("decode_layer outside decode_begin/end");
     check_layer(l);
     if (append_mode && !appended[l])
       throw layersim::SimulationError("decode_layer: append mode needs decode_append_layer first");
     const int st = l % cfg.pipeline_depth;
+    join_in(user);
     LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));
     const int n = static_cast<int>(members.size());
     if (timing) LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
@@ -931,6 +945,7 @@ struct lkv_device final : layersim::KvObserver {
     if (timing) LKV_CUDA(cudaEventRecord(t_attn1[l], cs));
     LKV_CUDA(cudaEventRecord(attn_done[st], cs));
     attn_recorded[st] = 1;
+    join_out(user);
     if (l + cfg.pipeline_depth < L) issue_fetch(l + cfg.pipeline_depth);
   }
 
@@ -1094,18 +1109,18 @@ int lkv_decode_begin_append(lkv_device* d, const int64_t* ids, int32_t n) {
   LKV_CATCH
 }
 
-int lkv_decode_append_layer(lkv_device* d, int32_t layer, const void* k_new, const void* v_new) {
+int lkv_decode_append_layer(lkv_device* d, int32_t layer, const void* k_new, const void* v_new, void* stream) {
   LKV_REQUIRE(d && d->kv && k_new && v_new);
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
-  d->decode_append_layer(layer, k_new, v_new);
+  d->decode_append_layer(layer, k_new, v_new, static_cast<cudaStream_t>(stream));
   LKV_CATCH
 }
 
 int lkv_decode_layer(lkv_device* d, int32_t layer, const void* q, void* out, float scale,
-                     int32_t out_dtype) {
+                     int32_t out_dtype, void* stream) {
   LKV_REQUIRE(d && q && out);
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
-  d->decode_layer(layer, q, out, scale, out_dtype == LKV_DTYPE_F32 ? 1 : 0);
+  d->decode_layer(layer, q, out, scale, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<cudaStream_t>(stream));
   LKV_CATCH
 }
 

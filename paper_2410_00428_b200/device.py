@@ -40,6 +40,18 @@ def _ptr(t) -> int:
     return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
 
 
+def _stream(stream):
+    """Caller's stream handle: the given torch stream, else torch's current
+    stream on the current device (so tensors produced there are ordered)."""
+    if stream is None:
+        try:
+            import torch
+            stream = torch.cuda.current_stream()
+        except Exception:
+            return None
+    return C.c_void_p(stream.cuda_stream)
+
+
 class Device:
     """One GPU's KV-head shard of the LayerKV data path, bound to a KvManager."""
 
@@ -87,15 +99,14 @@ class Device:
 
     # ------------------------------------------------------------- prefill
     def prefill_layer(self, request_id: int, layer: int, k, v, tokens: int, stream=None):
-        s = None if stream is None else C.c_void_p(stream.cuda_stream)
-        self._lib.call("lkv_prefill_layer", self.handle, request_id, layer, _ptr(k), _ptr(v), tokens, s)
+        self._lib.call("lkv_prefill_layer", self.handle, request_id, layer, _ptr(k), _ptr(v), tokens,
+                       _stream(stream))
 
     def prefill_attention(self, q, k, v, out, tokens: int, scale: float, out_dtype: int = DTYPE_BF16, stream=None):
         """Causal GQA attention of one prefill layer on the tensor cores:
         q/out [tokens][q_heads_local][d], k/v [tokens][kv_heads_local][d] (bf16; out bf16 or fp32)."""
-        s = None if stream is None else C.c_void_p(stream.cuda_stream)
         self._lib.call("lkv_prefill_attention", self.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(out), tokens, scale,
-                       out_dtype, s)
+                       out_dtype, _stream(stream))
 
     def prefill_offload_done(self, request_id: int) -> bool:
         out = C.c_int32()
@@ -117,11 +128,13 @@ class Device:
         arr = (C.c_int64 * max(1, len(request_ids)))(*request_ids)
         self._lib.call("lkv_decode_begin_append", self.handle, arr, len(request_ids))
 
-    def decode_append_layer(self, layer: int, k_new, v_new):
-        self._lib.call("lkv_decode_append_layer", self.handle, layer, _ptr(k_new), _ptr(v_new))
+    def decode_append_layer(self, layer: int, k_new, v_new, stream=None):
+        self._lib.call("lkv_decode_append_layer", self.handle, layer, _ptr(k_new), _ptr(v_new), _stream(stream))
 
-    def decode_layer(self, layer: int, q, out, scale: float, out_dtype: int = DTYPE_BF16):
-        self._lib.call("lkv_decode_layer", self.handle, layer, _ptr(q), _ptr(out), scale, out_dtype)
+    def decode_layer(self, layer: int, q, out, scale: float, out_dtype: int = DTYPE_BF16, stream=None):
+        """Paged attention of one layer; ordered after `stream`'s queued work
+        (default: torch's current stream), which in turn waits for `out`."""
+        self._lib.call("lkv_decode_layer", self.handle, layer, _ptr(q), _ptr(out), scale, out_dtype, _stream(stream))
 
     def decode_end(self):
         self._lib.call("lkv_decode_end", self.handle)

@@ -36,19 +36,61 @@ for r in rows[1:]:
     c = agg.setdefault(name, [0, 0.0])
     c[0] += 1
     c[1] += t
-STEP = ("decode_attn", "decode_merge", "decode_snapshot")
+STEP = ("decode_attn_v2", "decode_attn_kernel", "decode_merge", "decode_snapshot")
+ROWS = ("prefill_attn", "decode_gqa_tc")
 with open(os.path.join(out_dir, f"{tag}_launches.txt"), "w") as f:
     f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none of: python bench.py --steps 2 --warmup 1"
             f" --no-cpu-baseline\n# per-launch times are serialised/cold-cache: compare shares, not absolutes\n")
     for title, sel in (("decode-step kernels (the timed region)", lambda k: any(x in k for x in STEP)),
+                       ("tensor-core rows beside the headline (prefill attention, GQA decode tile)",
+                        lambda k: any(x in k for x in ROWS)),
                        ("setup kernels (prefill offload, synthetic data, verification)",
-                        lambda k: not any(x in k for x in STEP))):
+                        lambda k: not any(x in k for x in STEP + ROWS))):
         part = {k: v for k, v in agg.items() if sel(k)}
         total = sum(v[1] for v in part.values()) or 1.0
         f.write(f"\n## {title}\n{'kernel':50s} {'launches':>9s} {'total_us':>12s} {'avg_us':>10s} {'share':>7s}\n")
         for k, (n, t) in sorted(part.items(), key=lambda kv: -kv[1][1]):
             f.write(f"{k[:50]:50s} {n:9d} {t:12.1f} {t / n:10.2f} {100 * t / total:6.2f}%\n")
 print(open(os.path.join(out_dir, f"{tag}_launches.txt")).read())
+
+# ---- full captures of the tensor-core kernels (prefill attention, GQA decode tile)
+TC_KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+           "launch__registers_per_thread", "launch__grid_size", "launch__block_size",
+           "launch__shared_mem_per_block_dynamic", "smsp__inst_executed.sum",
+           "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
+           "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
+           "smsp__warp_issue_stalled_wait_per_warp_active.pct",
+           "smsp__warp_issue_stalled_math_pipe_throttle_per_warp_active.pct"]
+for cap in ("prefill_attn", "decode_gqa_tc"):
+    rep = os.path.join(ROOT, "gpurun_out", f"{cap}_{tag}.ncu-rep")
+    if not os.path.exists(rep):
+        continue
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rr = list(csv.reader(io.StringIO(raw)))
+    h, units = rr[0], rr[1]
+    lines = [f"# ncu --set full --clock-control none -k regex:{cap} (scripts/*_micro.py), tag {tag}"]
+    for r in rr[2:]:
+        for k in TC_KEYS + [x for x in h if "tensor" in x and "pct" in x and x not in TC_KEYS][:6]:
+            if k in h:
+                i = h.index(k)
+                lines.append(f"{k:70s} {r[i]} {units[i]}")
+        lines.append("")
+    sass = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                          capture_output=True, text=True).stdout
+    ops = collections.Counter()
+    for ln in sass.splitlines():
+        for m in ("UTCHMMA", "UTCBAR", "UTMALDG", "UBLKCP", "LDTM", "STTM", "MUFU.EX2", "HMMA"):
+            if m in ln:
+                ops[m] += 1
+    lines.append("# SASS opcodes present (static count in the source page): " +
+                 ", ".join(f"{k}={v}" for k, v in sorted(ops.items())))
+    with open(os.path.join(out_dir, f"{tag}_{cap}_ncu.txt"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    print("\n".join(lines))
 
 # ---- full capture of the decode kernel
 rep = os.path.join(ROOT, "gpurun_out", f"decode_attn_{tag}.ncu-rep")

@@ -76,6 +76,8 @@ def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=No
     dev.decode_end()
     dev.synchronize()
     worst = 0.0
+    limit = tol if tol is not None else (REL_TOL if out_dtype == DTYPE_F32 else 8e-3)
+    where = []
     for l in (layers if layers is not None else range(L)):
         got = outs[l].float().cpu().numpy()
         q16 = qs[l].view(torch.int16).numpy().view(np.uint16)
@@ -83,8 +85,14 @@ def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=No
             want = re.decode_attn_gen(seed, l, kv_lens[m], dev.head0, dev.kv_heads_local, group, q16[m], scale)
             err = np.abs(got[m] - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)
             worst = max(worst, float(err.max()))
-    limit = tol if tol is not None else (REL_TOL if out_dtype == DTYPE_F32 else 8e-3)
-    assert worst <= limit, f"attention rel err {worst:.3e} > {limit}"
+            if err.max() > limit:
+                h = int(np.argmax(err))
+                where.append(f"layer {l} member {m} (len {kv_lens[m]}) heads {np.nonzero(err > limit)[0].tolist()[:6]}"
+                             f" got {got[m, h, :3]} want {want[h, :3]}")
+    if where:  # diagnose: are the bytes themselves intact?
+        bad = [dev.verify_request(rid, kv_lens[m], seed) for m, rid in enumerate(ids)]
+        where.append(f"verify_request mismatches per member: {bad}")
+    assert worst <= limit, f"attention rel err {worst:.3e} > {limit}: " + "; ".join(where[:10])
     return worst, outs
 
 
