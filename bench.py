@@ -282,8 +282,11 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     L, bs, d, T = model.n_layers, 16, model.d_head, 16384
     nblk = T // bs
     kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model)
+    # staging: 64 x 16 MiB, enough to absorb the D2H backlog of a prompt whose
+    # per-layer offload is about as long as its per-layer compute
     dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=64, host_slots=nblk * L + 64,
-                                             arena_slots=64, max_requests=4, max_blocks=nblk + 8, max_batch=2))
+                                             arena_slots=64, max_requests=4, max_blocks=nblk + 8, max_batch=2,
+                                             staging_chunks=64, chunk_bytes=16 << 20))
     hq, hl = dev.q_heads_local, dev.kv_heads_local
     cs = dev.torch_stream("compute")
     g = torch.Generator(device=dev_t).manual_seed(3)
@@ -333,19 +336,21 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     }
 
 
-def gqa_decode_row(torch, dev_t, hbm_peak):
-    """a18 for the GQA configs (3/4): Llama-3-8B shape (Hq 32, Hkv 8), batch
-    16 x 32k context, layers GPU-resident, through the tcgen05 decode tile."""
+def gqa_decode_row(torch, dev_t, hbm_peak, hq=32, hkv=8, tp_size=1, B=16, ctx=32768, label="8B GQA"):
+    """a18 for the GQA configs: config 3 (Llama-3-8B shape, Hq 32 / Hkv 8) and
+    config 4's per-GPU shard (70B, Hq 64 / Hkv 8 at TP 8: one KV head and its
+    8 query heads on this rank), layers GPU-resident, through the tcgen05
+    decode tile."""
     from paper_2410_00428_b200 import layersim as ls
     from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
-    Lr, bs, B, ctx = 2, 16, 16, 32768
-    model = ls.ModelSpec(Lr, 32, 8, 128, 4096, 8.03e9, 2)
+    Lr, bs = 2, 16
+    model = ls.ModelSpec(Lr, hq, hkv, 128, hq * 128, 8.03e9, 2)
     nblk = ctx // bs
     slots = B * nblk * Lr
     kv = ls.KvManager(ls.BlockPools(slots + 64, 64, bs), model)
-    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=slots + 64, host_slots=64,
-                                             arena_slots=B * nblk + 8, max_requests=B + 1, max_blocks=nblk + 4,
-                                             max_batch=B))
+    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, tp_rank=0, tp_size=tp_size,
+                                             gpu_slots=slots + 64, host_slots=64, arena_slots=B * nblk + 8,
+                                             max_requests=B + 1, max_blocks=nblk + 4, max_batch=B))
     ids = list(range(B))
     for r in ids:
         assert kv.allocate_prefill(r, ctx, Lr)
@@ -363,9 +368,10 @@ def gqa_decode_row(torch, dev_t, hbm_peak):
         if it >= 1:
             ms = st.attn_ms / st.attn_launches
             best = ms if best is None else min(best, ms)
-    byts = B * ctx * ls.kv_bytes_per_token_layer(model)
+    byts = B * ctx * ls.kv_bytes_per_token_layer(model) // tp_size
     dev.close()
-    return {"kernel": "decode_gqa_tc_kernel (tcgen05, G=4) + merge", "shape": f"8B GQA batch {B} x {ctx}",
+    return {"kernel": f"decode_gqa_tc_kernel (tcgen05, G={hq // hkv}) + merge",
+            "shape": f"{label} batch {B} x {ctx}, kv heads on this GPU {hkv // tp_size}",
             "ms_per_layer": best, "gbs": byts / (best / 1e3) / 1e9, "peak": hbm_peak,
             "frac": byts / (best / 1e3) / 1e9 / hbm_peak}
 
@@ -559,6 +565,8 @@ def main():
         if world == 1 and not args.no_rows:  # §8 rows beside the headline (own devices, after this one is gone)
             rows = prefill_rows(torch, dev_t, link, tensor_peak())
             rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak)
+            rows["a18_gqa_decode_70b_tp8_shard"] = gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8, tp_size=8,
+                                                                  B=64, ctx=32768, label="70B GQA TP8 rank 0")
             line["rows"] = rows
         print(json.dumps(line), flush=True)
     if world > 1:
