@@ -1055,14 +1055,19 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
       !tc::make_map_3d(&km, k, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true) ||
       !tc::make_map_3d(&vm, v, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true))
     throw CudaError("prefill_attention: cuTensorMapEncodeTiled failed (pointers must be 16 B aligned)");
-  static bool attr_set = false;
-  if (!attr_set) {
-    LKV_CUDA(cudaFuncSetAttribute(prefill_attn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  PrefillAttnSmem::kBytes));
-    attr_set = true;
+  // LKV_PREFILL_WG=1: one softmax warpgroup per CTA (thread = whole row); default 2 (row split in halves)
+  static const int nwg = [] {
+    const char* e = std::getenv("LKV_PREFILL_WG");
+    return (e && std::atoi(e) == 1) ? 1 : 2;
+  }();
+  static bool attr_set[3] = {false, false, false};
+  auto fn = nwg == 1 ? prefill_attn_kernel<1> : prefill_attn_kernel<2>;
+  if (!attr_set[nwg]) {
+    LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, PrefillAttnSmem::kBytes));
+    attr_set[nwg] = true;
   }
   const dim3 grid(static_cast<unsigned>((tokens + 127) / 128), static_cast<unsigned>(d->Hql));
-  prefill_attn_kernel<<<grid, PrefillAttnSmem::kThreads, PrefillAttnSmem::kBytes, s>>>(
+  fn<<<grid, 64 + 128 * nwg, PrefillAttnSmem::kBytes, s>>>(
       qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
       scale * 1.4426950408889634f);
   LKV_CUDA(cudaGetLastError());

@@ -5,7 +5,7 @@
 // GQA decode tile.
 //
 // One CTA per (128-row query tile, query head), heaviest (diagonal-farthest)
-// tiles first. 192 threads:
+// tiles first. 64 + 128*NWG threads:
 //   warp 0     TMA producer: Q tile once, then K/V tiles {64 d, 1 head, 128 tok}
 //              through 3D tensor maps over [tokens][heads][128] (swizzle-128B,
 //              out-of-range tokens zero-filled) into a 2-stage ring;
@@ -13,8 +13,8 @@
 //              one of two TMEM S buffers; S(j+1) is issued as soon as K_{j+1}
 //              lands, so QK^T overlaps the softmax of tile j. O += P_j V_j
 //              accumulates in TMEM (P from smem K-major, V MN-major);
-//   warps 2-5  softmax: thread = query row = TMEM lane, the whole 128-column
-//              row in registers. Lazy rescaling: the running max only moves
+//   warps 2+   softmax: NWG warpgroups; thread = (query row = TMEM lane,
+//              column half), its 128/NWG columns of the row in registers. Lazy rescaling: the running max only moves
 //              when a tile exceeds it by more than 2^8, then the warp
 //              rescales its O rows in TMEM (ld/scale/st) before handing the
 //              next P over. P = hi + lo in bf16 (two MMAs into the same O):
@@ -37,11 +37,11 @@ struct PrefillAttnSmem {
   static constexpr int kStage = 65536;
   static constexpr int kPhi = kKV + 2 * kStage;  // 32 KiB: 2 halves (tok 0-63, 64-127)
   static constexpr int kPlo = kPhi + 32768;
-  static constexpr int kBar = kPlo + 32768;      // mbarriers
+  static constexpr int kRed = kPlo + 32768;      // [2 parity][2 halves][128 rows] f32 row maxima / sums
+  static constexpr int kBar = kRed + 2048;       // mbarriers
   static constexpr int kNumBars = 12;
   static constexpr int kTmem = kBar + kNumBars * 8;
-  static constexpr int kBytes = kTmem + 16 + 1024;  // + alignment slack
-  static constexpr int kThreads = 192;
+  static constexpr int kBytes = kTmem + 16;      // base is __align__(1024) (checked on entry)
   static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
 };
 
@@ -49,13 +49,20 @@ __device__ __forceinline__ void prefill_named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-__global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
+// NWG softmax warpgroups split each S row by columns (NWG=2: two threads per
+// query row, 64 columns each), doubling the softmax issue rate per SM; the
+// halves exchange row maxima through smem once per tile.
+template <int NWG>
+__global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
     float scale_log2) {
   using S = PrefillAttnSmem;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr int NSM = 128 * NWG;  // softmax threads
+  constexpr int CPT = 128 / NWG;  // S columns per softmax thread
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  if ((tc::saddr(sm) & 1023u) != 0u) __trap();  // swizzle-128B tiles need 1 KiB alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::kBar);
   uint64_t* q_full = bars;
   uint64_t* kv_full = bars + 1;   // [2]
@@ -78,9 +85,9 @@ __global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
       tc::bar_init(&kv_full[b], 1);
       tc::bar_init(&kv_empty[b], 1);
       tc::bar_init(&s_full[b], 1);
-      tc::bar_init(&s_empty[b], 128);
+      tc::bar_init(&s_empty[b], NSM);
     }
-    tc::bar_init(p_full, 128);
+    tc::bar_init(p_full, NSM);
     tc::bar_init(o_full, 1);
     tc::bar_fence_init();
   }
@@ -149,26 +156,35 @@ __global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
     }
   } else {
     const int quad = warp & 3;
+    const int wg = (warp - 2) >> 2;  // column half
     const int r = quad * 32 + lane;  // query row within the tile = TMEM lane
+    const int c0 = wg * CPT;
     const int row = qt * 128 + r;
     const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    float* red = reinterpret_cast<float*>(sm + S::kRed);
     float m_run = -INFINITY, l_run = 0.f;
-    float s[128];
+    float s[CPT];
     for (int j = 0; j < nt; ++j) {
       const int sb = j & 1;
       tc::bar_wait(&s_full[sb], (j >> 1) & 1u);
       tc::fence_after_sync();
 #pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tl + sb * 128 + c * 32, s + c * 32);
+      for (int c = 0; c < CPT / 32; ++c) tc::tmem_ld32(tl + sb * 128 + c0 + c * 32, s + c * 32);
       tc::tmem_wait_ld();
       tc::fence_before_sync();
       tc::bar_arrive(&s_empty[sb]);
       float mt = -INFINITY;
-      const int lim = (j == qt) ? r : 127;  // causal: key j*128+c <= row
+      const int lim = ((j == qt) ? r : 127) - c0;  // causal: key j*128+c0+c <= row
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
+      for (int c = 0; c < CPT; ++c) {
         s[c] = (c <= lim) ? s[c] * scale_log2 : -INFINITY;
         mt = fmaxf(mt, s[c]);
+      }
+      if constexpr (NWG > 1) {  // row max over both halves
+        float* rd = red + (j & 1) * 256;
+        rd[wg * 128 + r] = mt;
+        prefill_named_bar(1, NSM);
+        mt = fmaxf(mt, rd[(1 - wg) * 128 + r]);
       }
       // lazy rescale: move the reference max only when the tile exceeds it by > 2^8
       float corr = 1.f;
@@ -181,7 +197,7 @@ __global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
       }
       float ls = 0.f;
 #pragma unroll
-      for (int c = 0; c < 128; ++c) {
+      for (int c = 0; c < CPT; ++c) {
         s[c] = exp2f(s[c] - m_run);
         ls += s[c];
       }
@@ -190,22 +206,22 @@ __global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
         tc::bar_wait(o_full, (j - 1) & 1u);  // PV(j-1) done: O stable, P buffers free
         tc::fence_after_sync();
       }
-      if (__any_sync(0xffffffffu, resc)) {
+      if (__any_sync(0xffffffffu, resc)) {  // this half's O columns
         const float f = resc ? corr : 1.f;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < CPT / 32; ++c) {
           float o[32];
-          tc::tmem_ld32(tl + 256 + c * 32, o);
+          tc::tmem_ld32(tl + 256 + c0 + c * 32, o);
           tc::tmem_wait_ld();
 #pragma unroll
           for (int i = 0; i < 32; ++i) o[i] *= f;
-          tc::tmem_st32(tl + 256 + c * 32, o);
+          tc::tmem_st32(tl + 256 + c0 + c * 32, o);
         }
         tc::tmem_wait_st();
       }
-      // P row r: 16 x 16 B chunks, chunk c -> half c/8, swizzled position
+      // P row r, this half: 16 B chunk c (global chunk c0/8 + c) -> half, swizzled position
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < CPT / 8; ++c) {
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
@@ -213,7 +229,8 @@ __global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
           hi[i] = tc::pack_bf16(a, b);
           lo[i] = tc::pack_bf16(a - __uint_as_float(hi[i] << 16), b - __uint_as_float(hi[i] & 0xFFFF0000u));
         }
-        const uint32_t off = (c >> 3) * 16384 + tc::sw128_off(r, c & 7);
+        const int gc = c0 / 8 + c;
+        const uint32_t off = (gc >> 3) * 16384 + tc::sw128_off(r, gc & 7);
         *reinterpret_cast<uint4*>(sm + S::kPhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
         *reinterpret_cast<uint4*>(sm + S::kPlo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
       }
@@ -221,16 +238,22 @@ __global__ void __launch_bounds__(192, 1) prefill_attn_kernel(
       tc::fence_before_sync();
       tc::bar_arrive(p_full);
     }
+    if constexpr (NWG > 1) {  // row sum over both halves (same m_run in both)
+      float* rd = red + (nt & 1) * 256;
+      rd[wg * 128 + r] = l_run;
+      prefill_named_bar(1, NSM);
+      l_run += rd[(1 - wg) * 128 + r];
+    }
     tc::bar_wait(o_full, (nt - 1) & 1u);
     tc::fence_after_sync();
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    const long long obase = (static_cast<long long>(row) * Hq + hq) * 128;
+    const long long obase = (static_cast<long long>(row) * Hq + hq) * 128 + c0;
     __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + obase;
     float* dstf = static_cast<float*>(out) + obase;
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < CPT / 32; ++c) {
       float o[32];
-      tc::tmem_ld32(tl + 256 + c * 32, o);
+      tc::tmem_ld32(tl + 256 + c0 + c * 32, o);
       tc::tmem_wait_ld();
       if (row < tokens && out_f32) {
 #pragma unroll
