@@ -321,8 +321,9 @@ typedef struct lkv_decode_stats {
   int64_t attn_launches;
   int64_t kernel_launches;       /* every kernel this iteration launched (snapshot, attention, merge) */
   double attn_ms;               /* summed CUDA-event time of the attention launches */
-  double h2d_ms;                 /* CUDA-event span of the prefetch copies */
+  double h2d_ms;                 /* copy-engine busy time: summed CUDA-event time of each layer's prefetch copies */
   double iteration_ms;           /* decode_begin -> decode_end on the device */
+  double h2d_span_ms;            /* first prefetch copy start -> last prefetch copy end */
 } lkv_decode_stats;
 LKV_API int lkv_device_set_timing(lkv_device* dev, int32_t on);
 LKV_API int lkv_decode_last_stats(const lkv_device* dev, lkv_decode_stats* out);
@@ -330,7 +331,8 @@ LKV_API int lkv_decode_last_stats(const lkv_device* dev, lkv_decode_stats* out);
 typedef struct lkv_offload_stats {
   int64_t d2h_bytes_physical, d2h_bytes_algorithmic, d2h_copies, jobs;
   int64_t scatter_bytes;  /* slot bytes written by the scatter kernel */
-  double d2h_ms, pack_ms, scatter_ms;
+  double d2h_ms;                 /* copy-engine busy time of the D2H copies (timing on) */
+  double pack_ms, scatter_ms;
 } lkv_offload_stats;
 LKV_API int lkv_offload_last_stats(const lkv_device* dev, lkv_offload_stats* out, int32_t reset);
 

@@ -174,7 +174,8 @@ struct lkv_device final : layersim::KvObserver {
   int total_blocks = 0, max_nblk = 0;
   bool in_iteration = false;
   lkv_decode_stats dstats{};
-  std::vector<cudaEvent_t> t_attn0, t_attn1;
+  std::vector<cudaEvent_t> t_attn0, t_attn1, t_f0, t_f1;  // per layer: attention, prefetch copies
+  std::vector<char> fetched;
   cudaEvent_t t_it0 = nullptr, t_it1 = nullptr, t_h2d0 = nullptr, t_h2d1 = nullptr;
   bool h2d_started = false;
 
@@ -280,9 +281,14 @@ struct lkv_device final : layersim::KvObserver {
     }
     t_attn0.resize(L);
     t_attn1.resize(L);
+    t_f0.resize(L);
+    t_f1.resize(L);
+    fetched.assign(L, 0);
     for (int i = 0; i < L; ++i) {
       ev_create(&t_attn0[i], true);
       ev_create(&t_attn1[i], true);
+      ev_create(&t_f0[i], true);
+      ev_create(&t_f1[i], true);
     }
     ev_create(&t_it0, true);
     ev_create(&t_it1, true);
@@ -310,6 +316,9 @@ struct lkv_device final : layersim::KvObserver {
     kill(attn_done);
     kill(t_attn0);
     kill(t_attn1);
+    kill(t_f0);
+    kill(t_f1);
+    drain_timed(d2h_timed);
     for (auto e : {t_it0, t_it1, t_h2d0, t_h2d1, t_pack0, t_pack1, ev_join})
       if (e) cudaEventDestroy(e);
     for (auto& kvp : job_ev) cudaEventDestroy(kvp.second);
@@ -462,13 +471,42 @@ struct lkv_device final : layersim::KvObserver {
   }
 
   // Stream frames [i0, i0+n) of a staging producer to host frames cpu[...].
+  // Copy-engine busy time (timing on): event pairs around each batch of
+  // copies on a copy stream, summed when the stats are read.
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> d2h_timed;
+  void timed_begin(cudaStream_t st, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    cudaEvent_t a, b;
+    ev_create(&a, true);
+    ev_create(&b, true);
+    LKV_CUDA(cudaEventRecord(a, st));
+    v.push_back({a, b});
+  }
+  void timed_end(cudaStream_t st, std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    LKV_CUDA(cudaEventRecord(v.back().second, st));
+  }
+  static double drain_timed(std::vector<std::pair<cudaEvent_t, cudaEvent_t>>& v) {
+    double ms = 0.0;
+    for (auto& pr : v) {
+      float t = 0.f;
+      if (cudaEventSynchronize(pr.second) == cudaSuccess && cudaEventElapsedTime(&t, pr.first, pr.second) == cudaSuccess)
+        ms += t;
+      cudaEventDestroy(pr.first);
+      cudaEventDestroy(pr.second);
+    }
+    cudaGetLastError();
+    v.clear();
+    return ms;
+  }
+
   void d2h_segment(int seg, const long long* cpu_frames, long long n) {
     LKV_CUDA(cudaEventRecord(seg_ready[seg], cs));
     LKV_CUDA(cudaStreamWaitEvent(d2h, seg_ready[seg], 0));
     std::vector<long long> src(n);
     for (long long i = 0; i < n; ++i) src[i] = seg * seg_slots + i;
+    if (timing) timed_begin(d2h, d2h_timed);
     ostats.d2h_copies +=
         emit_copies(host_pool, cpu_frames, d_staging, src.data(), n, cudaMemcpyDeviceToHost, d2h);
+    if (timing) timed_end(d2h, d2h_timed);
     ostats.d2h_bytes_physical += n * sb;
     LKV_CUDA(cudaEventRecord(seg_free[seg], d2h));
   }
@@ -615,6 +653,8 @@ struct lkv_device final : layersim::KvObserver {
     }
     const long long arena0 = cfg.gpu_slots + static_cast<long long>(st) * cfg.arena_slots;
     std::vector<long long> src, dst;
+    const long long copies0 = dstats.h2d_copies;
+    if (timing) LKV_CUDA(cudaEventRecord(t_f0[l], h2d));
     for (const Member& m : members) {
       const RequestKv& r = kv->request(m.id);
       src.clear();
@@ -636,13 +676,18 @@ struct lkv_device final : layersim::KvObserver {
       dstats.h2d_bytes_algorithmic += tok * (sb / bs);
     }
     LKV_CUDA(cudaEventRecord(fetch_done[st], h2d));
-    if (timing) LKV_CUDA(cudaEventRecord(t_h2d1, h2d));
+    if (timing) {
+      LKV_CUDA(cudaEventRecord(t_f1[l], h2d));
+      fetched[l] = dstats.h2d_copies > copies0;
+      LKV_CUDA(cudaEventRecord(t_h2d1, h2d));
+    }
   }
 
   void decode_begin(const int64_t* ids, int n, bool append = false) {
     if (in_iteration) throw layersim::SimulationError("decode_begin: iteration already open");
     append_mode = append;
     appended.assign(L, 0);
+    fetched.assign(L, 0);
     if (n < 0 || n > cfg.max_batch) throw CapacityError("decode batch exceeds max_batch");
     flush();
     members.clear();
@@ -1156,8 +1201,13 @@ int lkv_decode_last_stats(const lkv_device* dc, lkv_decode_stats* out) {
     cudaGetLastError();
     out->attn_ms = attn;
     if (d->h2d_started && cudaEventElapsedTime(&ms, d->t_h2d0, d->t_h2d1) == cudaSuccess)
-      out->h2d_ms = ms;
+      out->h2d_span_ms = ms;
     cudaGetLastError();
+    double busy = 0.0;
+    for (int l = 0; l < d->L; ++l)
+      if (d->fetched[l] && cudaEventElapsedTime(&ms, d->t_f0[l], d->t_f1[l]) == cudaSuccess) busy += ms;
+    cudaGetLastError();
+    out->h2d_ms = busy;
     if (cudaEventElapsedTime(&ms, d->t_it0, d->t_it1) == cudaSuccess) out->iteration_ms = ms;
     cudaGetLastError();
   }
@@ -1167,9 +1217,11 @@ int lkv_decode_last_stats(const lkv_device* dc, lkv_decode_stats* out) {
 int lkv_offload_last_stats(const lkv_device* dc, lkv_offload_stats* out, int32_t reset) {
   LKV_REQUIRE(dc && out);
   lkv_device* d = const_cast<lkv_device*>(dc);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->ostats.d2h_ms += lkv_device::drain_timed(d->d2h_timed);
   *out = d->ostats;
   if (reset) d->ostats = lkv_offload_stats{};
-  return LKV_OK;
+  LKV_CATCH
 }
 
 int lkv_fill_kv(lkv_device* d, void* k, void* v, int64_t tokens, int64_t token0, int32_t layer,
