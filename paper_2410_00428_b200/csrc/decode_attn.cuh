@@ -19,7 +19,7 @@
 //    the log2 domain; P.V in fp32. G query heads of a GQA group share every
 //    K/V byte.
 //  * Each unit writes an unnormalised partial (m, l, o), merged per
-//    (sequence, query head) by decode_merge_v3_kernel (one warp each).
+//    (sequence, query head) by decode_merge_v4_kernel (one CTA each).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -366,6 +366,82 @@ __global__ void __launch_bounds__(128) decode_merge_v3_kernel(const float* __res
   const AttnSeq sd = seqs[m];
   merge_kv_head<32>(part_o, part_ml, sd.chunk0, sd.nchunk, h, Hl, G, (static_cast<long long>(m) * Hl + h) * G, out,
                     out_f32, threadIdx.x & 31, g, G);
+}
+
+// One CTA (4 warps) per (member, query head). Every warp finds the global max
+// over the chunks (lanes stride over chunks), then warp w folds chunks w,
+// w+4, ... with all its o-row loads issued before any FMA (8 in flight per
+// lane), and the four partial sums meet in shared memory.
+__global__ void __launch_bounds__(128) decode_merge_v4_kernel(const float* __restrict__ part_o,
+                                                              const float* __restrict__ part_ml,
+                                                              const AttnSeq* __restrict__ seqs, int Hl, int G,
+                                                              void* __restrict__ out, int out_f32) {
+  __shared__ float4 so[4][32];
+  __shared__ float sl[4];
+  const int m = blockIdx.x, hq = blockIdx.y, h = hq / G, g = hq % G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const AttnSeq sd = seqs[m];
+  const int nch = sd.nchunk;
+  const long long cstride = static_cast<long long>(Hl) * G;
+  const long long pu0 = (static_cast<long long>(sd.chunk0) * Hl + h) * G + g;
+  float M = -INFINITY;
+  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(part_ml + (pu0 + c * cstride) * 2));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float L = 0.f;
+  if (M != -INFINITY) {
+    for (int c0 = warp; c0 < nch; c0 += 4 * 8) {
+      float4 v[8];
+      float2 ml[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {  // issue every load of the batch first
+        const int c = c0 + 4 * i;
+        if (c < nch) {
+          const long long pu = pu0 + c * cstride;
+          v[i] = __ldcg(reinterpret_cast<const float4*>(part_o + pu * kHeadDim) + lane);
+          ml[i] = __ldcg(reinterpret_cast<const float2*>(part_ml + pu * 2));
+        } else {
+          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+          ml[i] = make_float2(-INFINITY, 0.f);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float f = (ml[i].x == -INFINITY) ? 0.f : exp2f(ml[i].x - M);
+        L = fmaf(f, ml[i].y, L);
+        acc.x = fmaf(f, v[i].x, acc.x);
+        acc.y = fmaf(f, v[i].y, acc.y);
+        acc.z = fmaf(f, v[i].z, acc.z);
+        acc.w = fmaf(f, v[i].w, acc.w);
+      }
+    }
+  }
+  so[warp][lane] = acc;
+  if (lane == 0) sl[warp] = L;
+  __syncthreads();
+  if (warp == 0) {
+    float4 r = so[0][lane];
+#pragma unroll
+    for (int w = 1; w < 4; ++w) {
+      r.x += so[w][lane].x;
+      r.y += so[w][lane].y;
+      r.z += so[w][lane].z;
+      r.w += so[w][lane].w;
+    }
+    const float Lt = sl[0] + sl[1] + sl[2] + sl[3];
+    const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
+    const long long idx = (static_cast<long long>(m) * Hl * G + hq) * kHeadDim + lane * 4;
+    if (out_f32) {
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + idx) = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
+    } else {
+      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + idx;
+      o[0] = __float2bfloat16_rn(r.x * inv);
+      o[1] = __float2bfloat16_rn(r.y * inv);
+      o[2] = __float2bfloat16_rn(r.z * inv);
+      o[3] = __float2bfloat16_rn(r.w * inv);
+    }
+  }
 }
 
 // Previous merge (one CTA per (member, query head), thread = dim).

@@ -133,7 +133,7 @@ struct lkv_device final : layersim::KvObserver {
   // bulk copies (decode_attn.cuh), 3 = tcgen05 GQA tile (decode_gqa_tc.cuh).
   // LKV_DECODE_KERNEL overrides the per-group-size default.
   int kernel_version = 2;
-  int merge_version = 3;           // LKV_MERGE=2: one CTA per (member, query head), thread = dim
+  int merge_version = 4;           // LKV_MERGE=2 / 3: earlier merge kernels (thread = dim / warp per head)
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
@@ -174,7 +174,7 @@ struct lkv_device final : layersim::KvObserver {
   int total_blocks = 0, max_nblk = 0;
   bool in_iteration = false;
   lkv_decode_stats dstats{};
-  std::vector<cudaEvent_t> t_attn0, t_attn1, t_f0, t_f1;  // per layer: attention, prefetch copies
+  std::vector<cudaEvent_t> t_attn0, t_attnk, t_attn1, t_f0, t_f1;  // per layer: attention | merge, prefetch copies
   std::vector<char> fetched;
   cudaEvent_t t_it0 = nullptr, t_it1 = nullptr, t_h2d0 = nullptr, t_h2d1 = nullptr;
   bool h2d_started = false;
@@ -241,7 +241,10 @@ struct lkv_device final : layersim::KvObserver {
       const int v = std::atoi(kv);
       kernel_version = (v == 1 || v == 3) ? v : 2;
     }
-    if (const char* mv = std::getenv("LKV_MERGE")) merge_version = std::atoi(mv) == 2 ? 2 : 3;
+    if (const char* mv = std::getenv("LKV_MERGE")) {
+      const int v = std::atoi(mv);
+      merge_version = (v == 2 || v == 3) ? v : 4;
+    }
     {
       const unsigned long long rows = static_cast<unsigned long long>(std::max<long long>(frames, 1)) * 2 * Hl * bs;
       if (rows > 0x7FFFFFFFull) throw CapacityError("pool + arena rows exceed the TMA coordinate range");
@@ -280,12 +283,14 @@ struct lkv_device final : layersim::KvObserver {
       ev_create(&attn_done[i]);
     }
     t_attn0.resize(L);
+    t_attnk.resize(L);
     t_attn1.resize(L);
     t_f0.resize(L);
     t_f1.resize(L);
     fetched.assign(L, 0);
     for (int i = 0; i < L; ++i) {
       ev_create(&t_attn0[i], true);
+      ev_create(&t_attnk[i], true);
       ev_create(&t_attn1[i], true);
       ev_create(&t_f0[i], true);
       ev_create(&t_f1[i], true);
@@ -315,6 +320,7 @@ struct lkv_device final : layersim::KvObserver {
     kill(fetch_done);
     kill(attn_done);
     kill(t_attn0);
+    kill(t_attnk);
     kill(t_attn1);
     kill(t_f0);
     kill(t_f1);
@@ -932,7 +938,10 @@ struct lkv_device final : layersim::KvObserver {
     join_in(user);
     LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[st], 0));
     const int n = static_cast<int>(members.size());
-    if (timing) LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
+    if (timing) {
+      LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
+      LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // re-recorded after the attention kernel when one runs
+    }
     if (n > 0 && kernel_version >= 2) {
       const float sl2 = scale * 1.4426950408889634f;
       if (n_chunks > 0 && kernel_version == 3) {
@@ -952,11 +961,14 @@ struct lkv_device final : layersim::KvObserver {
         }
         LKV_CUDA(cudaGetLastError());
       }
+      if (timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attention kernel | merge kernel
       // merge (members without KV get zero rows: no chunks, L = 0)
       if (merge_version == 2)
         decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
-      else
+      else if (merge_version == 3)
         decode_merge_v3_kernel<<<(n * Hql + 3) / 4, 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, n, Hl, G, out, f32);
+      else
+        decode_merge_v4_kernel<<<dim3(n, Hql), 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;
       dstats.kernel_launches += n_chunks > 0 ? 2 : 1;
@@ -980,6 +992,7 @@ struct lkv_device final : layersim::KvObserver {
         default: launch_attn_bs<8>(l, n_split, bps, q, out, f32, sl2); break;
       }
       LKV_CUDA(cudaGetLastError());
+      if (timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));
       dstats.attn_launches += 1;
       dstats.kernel_launches += n_split > 1 ? 2 : 1;
       if (n_split > 1) {
@@ -1194,12 +1207,14 @@ int lkv_decode_last_stats(const lkv_device* dc, lkv_decode_stats* out) {
   if (d->timing && !d->in_iteration) {
     LKV_CUDA(cudaEventSynchronize(d->t_it1));
     float ms = 0.f;
-    double attn = 0.0;
+    double attn = 0.0, merge = 0.0;
     for (int l = 0; l < d->L; ++l) {
-      if (cudaEventElapsedTime(&ms, d->t_attn0[l], d->t_attn1[l]) == cudaSuccess) attn += ms;
+      if (cudaEventElapsedTime(&ms, d->t_attn0[l], d->t_attnk[l]) == cudaSuccess) attn += ms;
+      if (cudaEventElapsedTime(&ms, d->t_attnk[l], d->t_attn1[l]) == cudaSuccess) merge += ms;
     }
     cudaGetLastError();
     out->attn_ms = attn;
+    out->merge_ms = merge;
     if (d->h2d_started && cudaEventElapsedTime(&ms, d->t_h2d0, d->t_h2d1) == cudaSuccess)
       out->h2d_span_ms = ms;
     cudaGetLastError();
