@@ -1125,7 +1125,7 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
     attr_set[nwg] = true;
   }
   const dim3 grid(static_cast<unsigned>((tokens + 127) / 128), static_cast<unsigned>(d->Hql));
-  fn<<<grid, 64 + 128 * nwg, PrefillAttnSmem::kBytes, s>>>(
+  fn<<<grid, 96 + 128 * nwg, PrefillAttnSmem::kBytes, s>>>(
       qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
       scale * 1.4426950408889634f);
   LKV_CUDA(cudaGetLastError());

@@ -5,20 +5,24 @@
 // GQA decode tile.
 //
 // One CTA per (128-row query tile, query head), heaviest (diagonal-farthest)
-// tiles first. 64 + 128*NWG threads:
-//   warp 0     TMA producer: Q tile once, then K/V tiles {64 d, 1 head, 128 tok}
-//              through 3D tensor maps over [tokens][heads][128] (swizzle-128B,
-//              out-of-range tokens zero-filled) into a 2-stage ring;
+// tiles first. 96 + 128*NWG threads:
+//   warp 0/2   TMA producers: Q once, then K (warp 0) and V (warp 2) tiles
+//              {64 d, 1 head, 128 tok} through 3D tensor maps over
+//              [tokens][heads][128] (swizzle-128B, out-of-range tokens
+//              zero-filled) into separate 2-stage rings. K frees at QK^T
+//              completion, V at PV completion, so neither waits behind the
+//              other and the next K load starts a full tile early;
 //   warp 1     MMA issuer + TMEM owner. S(j) = Q K_j^T (M=N=128, K=128) into
 //              one of two TMEM S buffers; S(j+1) is issued as soon as K_{j+1}
 //              lands, so QK^T overlaps the softmax of tile j. O += P_j V_j
 //              accumulates in TMEM (P from smem K-major, V MN-major);
-//   warps 2+   softmax: NWG warpgroups; thread = (query row = TMEM lane,
+//   warps 3+   softmax: NWG warpgroups; thread = (query row = TMEM lane,
 //              column half), its 128/NWG columns of the row in registers. Lazy rescaling: the running max only moves
 //              when a tile exceeds it by more than 2^8, then the warp
 //              rescales its O rows in TMEM (ld/scale/st) before handing the
 //              next P over. P = hi + lo in bf16 (two MMAs into the same O):
-//              ~2^-16 relative, inside the 1e-3 parity bar.
+//              2^-15 relative, inside the 1e-3 parity bar; the split is done
+//              with integer AND/PRMT so the XU pipe only runs ex2.
 // TMEM: S0 [0,128) S1 [128,256) O [256,384) of a 512-column allocation.
 #pragma once
 
@@ -39,11 +43,18 @@ struct PrefillAttnSmem {
   static constexpr int kPlo = kPhi + 32768;
   static constexpr int kRed = kPlo + 32768;      // [2 parity][2 halves][128 rows] f32 row maxima / sums
   static constexpr int kBar = kRed + 2048;       // mbarriers
-  static constexpr int kNumBars = 12;
+  static constexpr int kNumBars = 16;
   static constexpr int kTmem = kBar + kNumBars * 8;
   static constexpr int kBytes = kTmem + 16;      // base is __align__(1024) (checked on entry)
   static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
 };
+
+// 2^x on the MUFU pipe, flushing denormals (-inf -> +0).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 __device__ __forceinline__ void prefill_named_bar(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
@@ -53,7 +64,7 @@ __device__ __forceinline__ void prefill_named_bar(int id, int n) {
 // query row, 64 columns each), doubling the softmax issue rate per SM; the
 // halves exchange row maxima through smem once per tile.
 template <int NWG>
-__global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
+__global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
     float scale_log2) {
@@ -65,12 +76,14 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
   if ((tc::saddr(sm) & 1023u) != 0u) __trap();  // swizzle-128B tiles need 1 KiB alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::kBar);
   uint64_t* q_full = bars;
-  uint64_t* kv_full = bars + 1;   // [2]
-  uint64_t* kv_empty = bars + 3;  // [2]
+  uint64_t* k_full = bars + 1;    // [2] K ring: freed by QK^T
+  uint64_t* k_empty = bars + 3;   // [2]
   uint64_t* s_full = bars + 5;    // [2]
   uint64_t* s_empty = bars + 7;   // [2]
   uint64_t* p_full = bars + 9;
   uint64_t* o_full = bars + 10;
+  uint64_t* v_full = bars + 11;   // [2] V ring: freed by PV
+  uint64_t* v_empty = bars + 13;  // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S::kTmem);
 
   const int nq = (tokens + 127) / 128;
@@ -82,8 +95,10 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
   if (threadIdx.x == 0) {
     tc::bar_init(q_full, 1);
     for (int b = 0; b < 2; ++b) {
-      tc::bar_init(&kv_full[b], 1);
-      tc::bar_init(&kv_empty[b], 1);
+      tc::bar_init(&k_full[b], 1);
+      tc::bar_init(&k_empty[b], 1);
+      tc::bar_init(&v_full[b], 1);
+      tc::bar_init(&v_empty[b], 1);
       tc::bar_init(&s_full[b], 1);
       tc::bar_init(&s_empty[b], NSM);
     }
@@ -105,15 +120,24 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
       tc::bar_expect_tx(q_full, 32768);
       tc::tma_load_3d(sm + S::kQ, &qmap, 0, hq, qt * 128, q_full);
       tc::tma_load_3d(sm + S::kQ + 16384, &qmap, 64, hq, qt * 128, q_full);
+      for (int j = 0; j < nt; ++j) {  // K ring: a stage frees as soon as its QK^T completes
+        const int st = j & 1;
+        tc::bar_wait(&k_empty[st], ((j >> 1) & 1u) ^ 1u);
+        tc::bar_expect_tx(&k_full[st], 32768);
+        uint8_t* kt = sm + S::kKV + st * S::kStage;
+        tc::tma_load_3d(kt, &kmap, 0, h, j * 128, &k_full[st]);
+        tc::tma_load_3d(kt + 16384, &kmap, 64, h, j * 128, &k_full[st]);
+      }
+    }
+  } else if (warp == 2) {
+    if (lane == 0) {  // V ring: a stage frees when its PV completes, two tiles before it is needed again
       for (int j = 0; j < nt; ++j) {
         const int st = j & 1;
-        tc::bar_wait(&kv_empty[st], ((j >> 1) & 1u) ^ 1u);
-        tc::bar_expect_tx(&kv_full[st], 65536);
-        uint8_t* kt = sm + S::kKV + st * S::kStage;
-        tc::tma_load_3d(kt, &kmap, 0, h, j * 128, &kv_full[st]);
-        tc::tma_load_3d(kt + 16384, &kmap, 64, h, j * 128, &kv_full[st]);
-        tc::tma_load_3d(kt + 32768, &vmap, 0, h, j * 128, &kv_full[st]);
-        tc::tma_load_3d(kt + 49152, &vmap, 64, h, j * 128, &kv_full[st]);
+        tc::bar_wait(&v_empty[st], ((j >> 1) & 1u) ^ 1u);
+        tc::bar_expect_tx(&v_full[st], 32768);
+        uint8_t* vt = sm + S::kKV + st * S::kStage + 32768;
+        tc::tma_load_3d(vt, &vmap, 0, h, j * 128, &v_full[st]);
+        tc::tma_load_3d(vt + 16384, &vmap, 64, h, j * 128, &v_full[st]);
       }
     }
   } else if (warp == 1) {
@@ -123,6 +147,7 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
       const uint32_t q0 = tc::saddr(sm + S::kQ), kv0 = tc::saddr(sm + S::kKV);
       const uint32_t phi = tc::saddr(sm + S::kPhi), plo = tc::saddr(sm + S::kPlo);
       auto pv = [&](int i) {
+        tc::bar_wait(&v_full[i & 1], (i >> 1) & 1u);
         tc::bar_wait(p_full, i & 1u);
         tc::fence_after_sync();
         const uint32_t vt = kv0 + (i & 1) * S::kStage + 32768;
@@ -134,12 +159,12 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
           tc::mma_bf16(tmem + 256, tc::smem_desc(plo + ao, 16, 1024, tc::kLayoutSw128), bd, idO, 1u);
         }
         tc::mma_commit(o_full);
-        tc::mma_commit(&kv_empty[i & 1]);
+        tc::mma_commit(&v_empty[i & 1]);
       };
       tc::bar_wait(q_full, 0);
       for (int j = 0; j < nt; ++j) {
         const int st = j & 1;
-        tc::bar_wait(&kv_full[st], (j >> 1) & 1u);
+        tc::bar_wait(&k_full[st], (j >> 1) & 1u);
         tc::bar_wait(&s_empty[st], ((j >> 1) & 1u) ^ 1u);
         tc::fence_after_sync();
         const uint32_t kt = kv0 + st * S::kStage;
@@ -150,13 +175,14 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
                        tc::smem_desc(kt + o, 16, 1024, tc::kLayoutSw128), idS, kk > 0);
         }
         tc::mma_commit(&s_full[st]);
+        tc::mma_commit(&k_empty[st]);
         if (j > 0) pv(j - 1);
       }
       pv(nt - 1);
     }
   } else {
     const int quad = warp & 3;
-    const int wg = (warp - 2) >> 2;  // column half
+    const int wg = (warp - 3) >> 2;  // column half
     const int r = quad * 32 + lane;  // query row within the tile = TMEM lane
     const int c0 = wg * CPT;
     const int row = qt * 128 + r;
@@ -173,13 +199,17 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
       tc::tmem_wait_ld();
       tc::fence_before_sync();
       tc::bar_arrive(&s_empty[sb]);
-      float mt = -INFINITY;
-      const int lim = ((j == qt) ? r : 127) - c0;  // causal: key j*128+c0+c <= row
+      // raw scores: the max commutes with the positive scale, which is folded
+      // into the exponent's FMA below; only the diagonal tile is masked
+      if (j == qt) {
+        const int lim = r - c0;  // causal: key j*128+c0+c <= row
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        s[c] = (c <= lim) ? s[c] * scale_log2 : -INFINITY;
-        mt = fmaxf(mt, s[c]);
+        for (int c = 0; c < CPT; ++c) s[c] = (c <= lim) ? s[c] : -INFINITY;
       }
+      float mt = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < CPT; c += 2) mt = fmaxf(mt, fmaxf(s[c], s[c + 1]));
+      mt *= scale_log2;
       if constexpr (NWG > 1) {  // row max over both halves
         float* rd = red + (j & 1) * 256;
         rd[wg * 128 + r] = mt;
@@ -195,13 +225,15 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
         m_run = mt;
         l_run *= corr;
       }
-      float ls = 0.f;
+      float ls0 = 0.f, ls1 = 0.f;
 #pragma unroll
-      for (int c = 0; c < CPT; ++c) {
-        s[c] = exp2f(s[c] - m_run);
-        ls += s[c];
+      for (int c = 0; c < CPT; c += 2) {
+        s[c] = ex2_approx(fmaf(s[c], scale_log2, -m_run));
+        s[c + 1] = ex2_approx(fmaf(s[c + 1], scale_log2, -m_run));
+        ls0 += s[c];
+        ls1 += s[c + 1];
       }
-      l_run += ls;
+      l_run += ls0 + ls1;
       if (j > 0) {
         tc::bar_wait(o_full, (j - 1) & 1u);  // PV(j-1) done: O stable, P buffers free
         tc::fence_after_sync();
@@ -222,12 +254,17 @@ __global__ void __launch_bounds__(64 + 128 * NWG, 1) prefill_attn_kernel(
       // P row r, this half: 16 B chunk c (global chunk c0/8 + c) -> half, swizzled position
 #pragma unroll
       for (int c = 0; c < CPT / 8; ++c) {
+        // hi = p truncated to bf16, lo = (p - hi) truncated: hi + lo carries 16
+        // mantissa bits (2^-15 relative). Integer AND/PRMT only — the XU pipe
+        // (MUFU ex2 and F2F conversions) is this loop's bottleneck.
         uint32_t hi[4], lo[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
-          const float a = s[c * 8 + 2 * i], b = s[c * 8 + 2 * i + 1];
-          hi[i] = tc::pack_bf16(a, b);
-          lo[i] = tc::pack_bf16(a - __uint_as_float(hi[i] << 16), b - __uint_as_float(hi[i] & 0xFFFF0000u));
+          const uint32_t ua = __float_as_uint(s[c * 8 + 2 * i]), ub = __float_as_uint(s[c * 8 + 2 * i + 1]);
+          const float ra = s[c * 8 + 2 * i] - __uint_as_float(ua & 0xFFFF0000u);
+          const float rb = s[c * 8 + 2 * i + 1] - __uint_as_float(ub & 0xFFFF0000u);
+          hi[i] = __byte_perm(ua, ub, 0x7632);
+          lo[i] = __byte_perm(__float_as_uint(ra), __float_as_uint(rb), 0x7632);
         }
         const int gc = c0 / 8 + c;
         const uint32_t off = (gc >> 3) * 16384 + tc::sw128_off(r, gc & 7);
