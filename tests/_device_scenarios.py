@@ -112,8 +112,35 @@ def smoke_scenario(verbose=False):
         assert bad == 0, f"request {rid}: {bad} KV elements differ from the generator"
     worst, _ = check_attention(dev, [0, 1, 2], [100, 37, 200])
     st = dev.decode_stats()
+    pworst = check_prefill_attention(dev, 200)
     if verbose:
-        print(f"smoke: bytes bit-exact; attention max rel err {worst:.2e}; "
+        print(f"smoke: bytes bit-exact; decode attention (tcgen05 GQA tile) max rel err {worst:.2e}; "
+              f"prefill attention (tcgen05) max rel err {pworst:.2e}; "
               f"h2d {st.h2d_bytes_physical} B in {st.h2d_copies} copies; {st.attn_launches} attention launches")
     dev.close()
-    return worst
+    return max(worst, pworst)
+
+
+def check_prefill_attention(dev, T, seed=SEED):
+    """Causal prefill attention of generator K/V (layer 0) through
+    lkv_prefill_attention vs the fp64 oracle, fp32 output, 1e-3 relative."""
+    import torch
+    import oracle
+    re = oracle.restatement()
+    hq, hl, d = dev.q_heads_local, dev.kv_heads_local, dev.head_dim
+    k = torch.empty((T, hl, d), dtype=torch.bfloat16, device="cuda:0")
+    v = torch.empty_like(k)
+    s = dev.torch_stream("compute")
+    dev.fill_kv(k, v, T, 0, 0, seed, stream=s)
+    q = random_q(T, hq, d, 4242).to("cuda:0")
+    out = torch.empty((T, hq, d), dtype=torch.float32, device="cuda:0")
+    torch.cuda.synchronize()
+    dev.prefill_attention(q, k, v, out, T, 1.0 / math.sqrt(d), DTYPE_F32, stream=s)
+    dev.synchronize()
+    want = re.prefill_attn(q.cpu().view(torch.int16).numpy().view(np.uint16),
+                           k.cpu().view(torch.int16).numpy().view(np.uint16),
+                           v.cpu().view(torch.int16).numpy().view(np.uint16), 1.0 / math.sqrt(d))
+    got = out.cpu().numpy()
+    err = float((np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)).max())
+    assert err <= REL_TOL, f"prefill attention rel err {err:.3e} > {REL_TOL}"
+    return err
