@@ -758,7 +758,15 @@ struct lkv_device final : layersim::KvObserver {
     const int tile_blocks = 128 / bs;
     int cb = tc_path ? 16 * tile_blocks : 32;
     const int cb_min = tc_path ? tile_blocks : 1;
-    while (cb > cb_min && block_heads / cb < 8 * workers) cb >>= 1;
+    // units per worker before halving the chunk: the tensor-core kernel's
+    // per-unit epilogue favours fewer, longer units (measured: 4 -> 85%, 8 ->
+    // 81% on the 70B TP8 shard; flat on 8B), the CUDA-core one balances at 8.
+    static const long long env_per_worker = [] {
+      const char* e = std::getenv("LKV_UNITS_PER_WORKER");
+      return e ? std::max(1ll, std::atoll(e)) : 0ll;
+    }();
+    const long long per_worker = env_per_worker ? env_per_worker : (tc_path ? 4 : 8);
+    while (cb > cb_min && block_heads / cb < per_worker * workers) cb >>= 1;
     std::vector<AttnChunk> ch;
     auto* aseq = reinterpret_cast<AttnSeq*>(ring.reserve(std::max<std::size_t>(members.size(), 1) * sizeof(AttnSeq)));
     for (std::size_t i = 0; i < members.size(); ++i) {
