@@ -18,6 +18,7 @@
 #include <sstream>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 #include <cstdlib>
@@ -806,17 +807,22 @@ struct lkv_device final : layersim::KvObserver {
   // G>=2 keeps 8x3 (register-limited to 8 warps).
   static int v2_warps(int g) { return g == 1 ? 12 : 8; }
 
+  // Opt-in dynamic shared memory, once per kernel on this device (the
+  // attribute is per device context, so it is tracked per lkv_device).
+  std::unordered_set<const void*> smem_attr_done;
+  void smem_attr(const void* fn, int bytes) {
+    if (smem_attr_done.count(fn)) return;
+    LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    smem_attr_done.insert(fn);
+  }
+
   // ---- v3: tcgen05 GQA tile (decode_gqa_tc.cuh) -------------------------------
   template <int GG, int BB>
   void launch_tc(int l, const void* q, float sl2, void* out, int f32) {
     constexpr int NS = 3;
     using K = GqaTc<GG, BB, NS>;
     auto fn = decode_gqa_tc_kernel<GG, BB, NS>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-      LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem));
-      attr_set = true;
-    }
+    smem_attr(reinterpret_cast<const void*>(fn), K::kSmem);
     const int units = n_chunks * Hl;
     const int grid = std::max(1, std::min(sms, units));
     fn<<<grid, K::kThreads, K::kSmem, cs>>>(kvmap, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
@@ -835,11 +841,7 @@ struct lkv_device final : layersim::KvObserver {
   void launch_v2_cfg(int l, const void* q, float sl2, void* out, int f32) {
     using K = AttnV2<GG, BB, W, S>;
     auto fn = decode_attn_v2_kernel<GG, BB, W, S>;
-    static bool attr_set = false;  // per instantiation
-    if (!attr_set) {
-      LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, K::kSmem));
-      attr_set = true;
-    }
+    smem_attr(reinterpret_cast<const void*>(fn), K::kSmem);
     const int units = n_chunks * Hl;
     const int grid = std::max(1, std::min(sms, (units + W - 1) / W));
     fn<<<grid, K::kThreads, K::kSmem, cs>>>(dbuf, sb, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
@@ -1126,12 +1128,8 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
     const char* e = std::getenv("LKV_PREFILL_WG");
     return (e && std::atoi(e) == 1) ? 1 : 2;
   }();
-  static bool attr_set[3] = {false, false, false};
   auto fn = nwg == 1 ? prefill_attn_kernel<1> : prefill_attn_kernel<2>;
-  if (!attr_set[nwg]) {
-    LKV_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, PrefillAttnSmem::kBytes));
-    attr_set[nwg] = true;
-  }
+  d->smem_attr(reinterpret_cast<const void*>(fn), PrefillAttnSmem::kBytes);
   const dim3 grid(static_cast<unsigned>((tokens + 127) / 128), static_cast<unsigned>(d->Hql));
   fn<<<grid, 96 + 128 * nwg, PrefillAttnSmem::kBytes, s>>>(
       qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
