@@ -9,21 +9,25 @@
 //   warp 0/2   TMA producers: Q once, then K (warp 0) and V (warp 2) tiles
 //              {64 d, 1 head, 128 tok} through 3D tensor maps over
 //              [tokens][heads][128] (swizzle-128B, out-of-range tokens
-//              zero-filled) into separate 2-stage rings. K frees at QK^T
+//              zero-filled) into separate 3-stage rings. K frees at QK^T
 //              completion, V at PV completion, so neither waits behind the
-//              other and the next K load starts a full tile early;
+//              other and loads run up to two tiles ahead;
 //   warp 1     MMA issuer + TMEM owner. S(j) = Q K_j^T (M=N=128, K=128) into
 //              one of two TMEM S buffers; S(j+1) is issued as soon as K_{j+1}
 //              lands, so QK^T overlaps the softmax of tile j. O += P_j V_j
-//              accumulates in TMEM (P from smem K-major, V MN-major);
+//              accumulates in TMEM with P read from TMEM (the "TS" form: P
+//              overwrites its own S buffer) and V MN-major from smem;
 //   warps 3+   softmax: NWG warpgroups; thread = (query row = TMEM lane,
-//              column half), its 128/NWG columns of the row in registers. Lazy rescaling: the running max only moves
-//              when a tile exceeds it by more than 2^8, then the warp
-//              rescales its O rows in TMEM (ld/scale/st) before handing the
-//              next P over. P = hi + lo in bf16 (two MMAs into the same O):
-//              2^-15 relative, inside the 1e-3 parity bar; the split is done
-//              with integer AND/PRMT so the XU pipe only runs ex2.
-// TMEM: S0 [0,128) S1 [128,256) O [256,384) of a 512-column allocation.
+//              column half), its 128/NWG columns of the row in registers.
+//              Lazy rescaling: the running max only moves when a tile
+//              exceeds it by more than 2^8; only then does the warp wait for
+//              the previous PV and rescale its O columns in TMEM. P = hi + lo
+//              in bf16 (two MMAs into the same O): 2^-15 relative, inside the
+//              1e-3 parity bar; the split is integer AND/PRMT so the XU pipe
+//              only runs ex2.
+// TMEM: S0/P0 [0,128) S1/P1 [128,256) O [256,384) of a 512-column allocation;
+// P of tile j sits in S(j)'s columns: hi [0,64), lo [64,128), two bf16 per
+// column (K = token pairs), 8 columns per K=16 MMA step.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -36,16 +40,15 @@
 namespace lkv {
 
 struct PrefillAttnSmem {
-  static constexpr int kQ = 0;               // 32 KiB: 2 SW128 halves (d 0-63, 64-127)
-  static constexpr int kKV = 32768;          // 2 stages x (K 32 KiB | V 32 KiB)
-  static constexpr int kStage = 65536;
-  static constexpr int kPhi = kKV + 2 * kStage;  // 32 KiB: 2 halves (tok 0-63, 64-127)
-  static constexpr int kPlo = kPhi + 32768;
-  static constexpr int kRed = kPlo + 32768;      // [2 parity][2 halves][128 rows] f32 row maxima / sums
-  static constexpr int kBar = kRed + 2048;       // mbarriers
-  static constexpr int kNumBars = 16;
+  static constexpr int kStages = 3;
+  static constexpr int kQ = 0;                       // 32 KiB: 2 SW128 halves (d 0-63, 64-127)
+  static constexpr int kK = 32768;                   // kStages x 32 KiB
+  static constexpr int kV = kK + kStages * 32768;    // kStages x 32 KiB
+  static constexpr int kRed = kV + kStages * 32768;  // [2 parity][2 halves][128 rows] f32 row maxima / sums
+  static constexpr int kBar = kRed + 2048;           // mbarriers
+  static constexpr int kNumBars = 8 + 4 * kStages;
   static constexpr int kTmem = kBar + kNumBars * 8;
-  static constexpr int kBytes = kTmem + 16;      // base is __align__(1024) (checked on entry)
+  static constexpr int kBytes = kTmem + 16;          // base is __align__(1024) (checked on entry)
   static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
 };
 
@@ -69,6 +72,7 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
     float scale_log2) {
   using S = PrefillAttnSmem;
+  constexpr int NS = S::kStages;
   constexpr int NSM = 128 * NWG;  // softmax threads
   constexpr int CPT = 128 / NWG;  // S columns per softmax thread
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -76,14 +80,14 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
   if ((tc::saddr(sm) & 1023u) != 0u) __trap();  // swizzle-128B tiles need 1 KiB alignment
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::kBar);
   uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;    // [2] K ring: freed by QK^T
-  uint64_t* k_empty = bars + 3;   // [2]
-  uint64_t* s_full = bars + 5;    // [2]
-  uint64_t* s_empty = bars + 7;   // [2]
-  uint64_t* p_full = bars + 9;
-  uint64_t* o_full = bars + 10;
-  uint64_t* v_full = bars + 11;   // [2] V ring: freed by PV
-  uint64_t* v_empty = bars + 13;  // [2]
+  uint64_t* s_full = bars + 1;    // [2] S(j) in TMEM
+  uint64_t* s_empty = bars + 3;   // [2] S(j) read into registers
+  uint64_t* p_full = bars + 5;    //     P(j) in TMEM
+  uint64_t* o_full = bars + 6;    //     PV(j) done
+  uint64_t* k_full = bars + 8;    // [NS] K ring: freed by QK^T
+  uint64_t* k_empty = k_full + NS;
+  uint64_t* v_full = k_empty + NS;  // [NS] V ring: freed by PV
+  uint64_t* v_empty = v_full + NS;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S::kTmem);
 
   const int nq = (tokens + 127) / 128;
@@ -95,12 +99,14 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
   if (threadIdx.x == 0) {
     tc::bar_init(q_full, 1);
     for (int b = 0; b < 2; ++b) {
+      tc::bar_init(&s_full[b], 1);
+      tc::bar_init(&s_empty[b], NSM);
+    }
+    for (int b = 0; b < NS; ++b) {
       tc::bar_init(&k_full[b], 1);
       tc::bar_init(&k_empty[b], 1);
       tc::bar_init(&v_full[b], 1);
       tc::bar_init(&v_empty[b], 1);
-      tc::bar_init(&s_full[b], 1);
-      tc::bar_init(&s_empty[b], NSM);
     }
     tc::bar_init(p_full, NSM);
     tc::bar_init(o_full, 1);
@@ -116,26 +122,26 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
     if (lane == 0) {
       tc::tma_prefetch_desc(&qmap);
       tc::tma_prefetch_desc(&kmap);
-      tc::tma_prefetch_desc(&vmap);
       tc::bar_expect_tx(q_full, 32768);
       tc::tma_load_3d(sm + S::kQ, &qmap, 0, hq, qt * 128, q_full);
       tc::tma_load_3d(sm + S::kQ + 16384, &qmap, 64, hq, qt * 128, q_full);
       for (int j = 0; j < nt; ++j) {  // K ring: a stage frees as soon as its QK^T completes
-        const int st = j & 1;
-        tc::bar_wait(&k_empty[st], ((j >> 1) & 1u) ^ 1u);
+        const int st = j % NS;
+        tc::bar_wait(&k_empty[st], ((j / NS) & 1u) ^ 1u);
         tc::bar_expect_tx(&k_full[st], 32768);
-        uint8_t* kt = sm + S::kKV + st * S::kStage;
+        uint8_t* kt = sm + S::kK + st * 32768;
         tc::tma_load_3d(kt, &kmap, 0, h, j * 128, &k_full[st]);
         tc::tma_load_3d(kt + 16384, &kmap, 64, h, j * 128, &k_full[st]);
       }
     }
   } else if (warp == 2) {
-    if (lane == 0) {  // V ring: a stage frees when its PV completes, two tiles before it is needed again
+    if (lane == 0) {  // V ring: a stage frees when its PV completes
+      tc::tma_prefetch_desc(&vmap);
       for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        tc::bar_wait(&v_empty[st], ((j >> 1) & 1u) ^ 1u);
+        const int st = j % NS;
+        tc::bar_wait(&v_empty[st], ((j / NS) & 1u) ^ 1u);
         tc::bar_expect_tx(&v_full[st], 32768);
-        uint8_t* vt = sm + S::kKV + st * S::kStage + 32768;
+        uint8_t* vt = sm + S::kV + st * 32768;
         tc::tma_load_3d(vt, &vmap, 0, h, j * 128, &v_full[st]);
         tc::tma_load_3d(vt + 16384, &vmap, 64, h, j * 128, &v_full[st]);
       }
@@ -144,38 +150,40 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
       constexpr uint32_t idO = tc::idesc_bf16(128, 128, false, true);
-      const uint32_t q0 = tc::saddr(sm + S::kQ), kv0 = tc::saddr(sm + S::kKV);
-      const uint32_t phi = tc::saddr(sm + S::kPhi), plo = tc::saddr(sm + S::kPlo);
+      const uint32_t q0 = tc::saddr(sm + S::kQ), k0 = tc::saddr(sm + S::kK), v0 = tc::saddr(sm + S::kV);
+      // PV(i) reads P(i) from S(i)'s TMEM columns; it is issued before
+      // S(i+2) (same columns), and tcgen05.mma executes in issue order.
       auto pv = [&](int i) {
-        tc::bar_wait(&v_full[i & 1], (i >> 1) & 1u);
+        const int vs = i % NS;
+        tc::bar_wait(&v_full[vs], (i / NS) & 1u);
         tc::bar_wait(p_full, i & 1u);
         tc::fence_after_sync();
-        const uint32_t vt = kv0 + (i & 1) * S::kStage + 32768;
+        const uint32_t vt = v0 + vs * 32768;
+        const uint32_t pt = tmem + (i & 1) * 128;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t bd = tc::smem_desc(vt + kk * 2048, 16384, 1024, tc::kLayoutSw128);
-          const uint32_t ao = (kk >> 2) * 16384 + (kk & 3) * 32;
-          tc::mma_bf16(tmem + 256, tc::smem_desc(phi + ao, 16, 1024, tc::kLayoutSw128), bd, idO, (i > 0 || kk > 0));
-          tc::mma_bf16(tmem + 256, tc::smem_desc(plo + ao, 16, 1024, tc::kLayoutSw128), bd, idO, 1u);
+          tc::mma_bf16_ts(tmem + 256, pt + kk * 8, bd, idO, (i > 0 || kk > 0));
+          tc::mma_bf16_ts(tmem + 256, pt + 64 + kk * 8, bd, idO, 1u);
         }
         tc::mma_commit(o_full);
-        tc::mma_commit(&v_empty[i & 1]);
+        tc::mma_commit(&v_empty[vs]);
       };
       tc::bar_wait(q_full, 0);
       for (int j = 0; j < nt; ++j) {
-        const int st = j & 1;
-        tc::bar_wait(&k_full[st], (j >> 1) & 1u);
-        tc::bar_wait(&s_empty[st], ((j >> 1) & 1u) ^ 1u);
+        const int sb = j & 1, ks = j % NS;
+        tc::bar_wait(&k_full[ks], (j / NS) & 1u);
+        tc::bar_wait(&s_empty[sb], ((j >> 1) & 1u) ^ 1u);
         tc::fence_after_sync();
-        const uint32_t kt = kv0 + st * S::kStage;
+        const uint32_t kt = k0 + ks * 32768;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
           const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
-          tc::mma_bf16(tmem + st * 128, tc::smem_desc(q0 + o, 16, 1024, tc::kLayoutSw128),
+          tc::mma_bf16(tmem + sb * 128, tc::smem_desc(q0 + o, 16, 1024, tc::kLayoutSw128),
                        tc::smem_desc(kt + o, 16, 1024, tc::kLayoutSw128), idS, kk > 0);
         }
-        tc::mma_commit(&s_full[st]);
-        tc::mma_commit(&k_empty[st]);
+        tc::mma_commit(&s_full[sb]);
+        tc::mma_commit(&k_empty[ks]);
         if (j > 0) pv(j - 1);
       }
       pv(nt - 1);
@@ -210,7 +218,7 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
 #pragma unroll
       for (int c = 0; c < CPT; c += 2) mt = fmaxf(mt, fmaxf(s[c], s[c + 1]));
       mt *= scale_log2;
-      if constexpr (NWG > 1) {  // row max over both halves
+      if constexpr (NWG > 1) {  // row max over both halves; also orders every S load before any P store
         float* rd = red + (j & 1) * 256;
         rd[wg * 128 + r] = mt;
         prefill_named_bar(1, NSM);
@@ -234,11 +242,9 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
         ls1 += s[c + 1];
       }
       l_run += ls0 + ls1;
-      if (j > 0) {
-        tc::bar_wait(o_full, (j - 1) & 1u);  // PV(j-1) done: O stable, P buffers free
+      if (__any_sync(0xffffffffu, resc)) {  // O must hold PV(j-1) before it is rescaled
+        tc::bar_wait(o_full, (j - 1) & 1u);
         tc::fence_after_sync();
-      }
-      if (__any_sync(0xffffffffu, resc)) {  // this half's O columns
         const float f = resc ? corr : 1.f;
 #pragma unroll 1
         for (int c = 0; c < CPT / 32; ++c) {
@@ -249,29 +255,27 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
           for (int i = 0; i < 32; ++i) o[i] *= f;
           tc::tmem_st32(tl + 256 + c0 + c * 32, o);
         }
-        tc::tmem_wait_st();
       }
-      // P row r, this half: 16 B chunk c (global chunk c0/8 + c) -> half, swizzled position
+      // P(j) -> TMEM over S(j): hi = p truncated to bf16, lo = (p - hi)
+      // truncated; tokens c0+2i, c0+2i+1 -> column (c0/2 + i), low half even.
+      // Buffer j&1 was last read by PV(j-2), which completed before S(j) was
+      // written (in-order tensor pipe).
 #pragma unroll
-      for (int c = 0; c < CPT / 8; ++c) {
-        // hi = p truncated to bf16, lo = (p - hi) truncated: hi + lo carries 16
-        // mantissa bits (2^-15 relative). Integer AND/PRMT only — the XU pipe
-        // (MUFU ex2 and F2F conversions) is this loop's bottleneck.
-        uint32_t hi[4], lo[4];
+      for (int c = 0; c < CPT / 32; ++c) {
+        uint32_t hi[16], lo[16];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const uint32_t ua = __float_as_uint(s[c * 8 + 2 * i]), ub = __float_as_uint(s[c * 8 + 2 * i + 1]);
-          const float ra = s[c * 8 + 2 * i] - __uint_as_float(ua & 0xFFFF0000u);
-          const float rb = s[c * 8 + 2 * i + 1] - __uint_as_float(ub & 0xFFFF0000u);
+        for (int i = 0; i < 16; ++i) {
+          const float a = s[c * 32 + 2 * i], b = s[c * 32 + 2 * i + 1];
+          const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+          const float ra = a - __uint_as_float(ua & 0xFFFF0000u), rb = b - __uint_as_float(ub & 0xFFFF0000u);
           hi[i] = __byte_perm(ua, ub, 0x7632);
           lo[i] = __byte_perm(__float_as_uint(ra), __float_as_uint(rb), 0x7632);
         }
-        const int gc = c0 / 8 + c;
-        const uint32_t off = (gc >> 3) * 16384 + tc::sw128_off(r, gc & 7);
-        *reinterpret_cast<uint4*>(sm + S::kPhi + off) = make_uint4(hi[0], hi[1], hi[2], hi[3]);
-        *reinterpret_cast<uint4*>(sm + S::kPlo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+        const uint32_t col = sb * 128 + c0 / 2 + c * 16;
+        tc::tmem_st16(tl + col, hi);
+        tc::tmem_st16(tl + col + 64, lo);
       }
-      tc::fence_async_smem();
+      tc::tmem_wait_st();
       tc::fence_before_sync();
       tc::bar_arrive(p_full);
     }

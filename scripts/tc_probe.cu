@@ -4,6 +4,7 @@
 //   T2  O^T[128x16]  = V^T (MN-major SW128, TMA) . P^T (MN-major none)
 //   T3  S[128x128]   = Q (K-major SW128, TMA) . K^T (K-major SW128, TMA)
 //   T4  O[128x128]   = P (K-major SW128, st.shared) . V (MN-major SW128, TMA)
+//   T5  O[128x128]   = P (TMEM, tcgen05.st; TS form) . V (MN-major SW128, TMA)
 // Build: nvcc -std=c++17 -O2 -gencode arch=compute_100a,code=sm_100a -I paper_2410_00428_b200/csrc
 //        scripts/tc_probe.cu -o build/tc_probe
 #include <cuda_bf16.h>
@@ -45,7 +46,7 @@ __global__ void __launch_bounds__(128, 1)
     bar_init(&s.bar_mma, 1);
     bar_fence_init();
   }
-  if (warp == 0) tmem_alloc<128>(&s.tmem);
+  if (warp == 0) tmem_alloc<256>(&s.tmem);
   fence_before_sync();
   __syncthreads();
   fence_after_sync();
@@ -66,7 +67,7 @@ __global__ void __launch_bounds__(128, 1)
         tma_load_2d(s.a + h * 16384, &mapA, h * 64, 0, &s.bar_tma);
         tma_load_2d(s.b + h * 16384, &mapB, h * 64, 0, &s.bar_tma);
       }
-    } else {
+    } else {  // T4, T5: V from A's data
       tx = 32768;
       bar_expect_tx(&s.bar_tma, tx);
       for (int h = 0; h < 2; ++h) tma_load_2d(s.b + h * 16384, &mapA, h * 64, 0, &s.bar_tma);
@@ -87,6 +88,15 @@ __global__ void __launch_bounds__(128, 1)
       *reinterpret_cast<__nv_bfloat16*>(s.b + (t / 8) * 256 + (g / 8) * 128 + (t % 8) * 16 + (g % 8) * 2) =
           bsrc[i];
     }
+  } else if (TEST == 5) {
+    // P [128 q][128 tok] -> TMEM columns [128, 192): lane = row, two bf16 per column
+    const uint32_t lane_addr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + 128;
+    for (int c = 0; c < 4; ++c) {
+      uint32_t v[16];
+      for (int i = 0; i < 16; ++i) v[i] = *reinterpret_cast<const uint32_t*>(bsrc + tid * 128 + c * 32 + 2 * i);
+      tmem_st16(lane_addr + c * 16, v);
+    }
+    tmem_wait_st();
   } else if (TEST == 4) {
     // P [128 q][128 tok] -> K-major SW128, thread = row
     const int r = tid;
@@ -96,7 +106,9 @@ __global__ void __launch_bounds__(128, 1)
     }
   }
   fence_async_smem();
+  fence_before_sync();
   __syncthreads();
+  fence_after_sync();
 
   if (tid == 0) {
     bar_wait(&s.bar_tma, 0);
@@ -122,7 +134,10 @@ __global__ void __launch_bounds__(128, 1)
         bd = smem_desc(b0 + kk * 2048, 16384, 1024, kLayoutSw128);
         id = idesc_bf16(128, 128, false, true);
       }
-      mma_bf16(tmem, ad, bd, id, kk > 0);
+      if (TEST == 5)
+        mma_bf16_ts(tmem, tmem + 128 + kk * 8, bd, id, kk > 0);
+      else
+        mma_bf16(tmem, ad, bd, id, kk > 0);
     }
     mma_commit(&s.bar_mma);
   }
@@ -139,7 +154,7 @@ __global__ void __launch_bounds__(128, 1)
   }
   fence_before_sync();
   __syncthreads();
-  if (warp == 0) tmem_free<128>(tmem);
+  if (warp == 0) tmem_free<256>(tmem);
 }
 
 static float bf(const __nv_bfloat16& x) { return __bfloat162float(x); }
@@ -168,7 +183,7 @@ int main() {
   }
   const size_t smem = sizeof(Smem) + 1024;
   int fails = 0;
-  for (int test = 1; test <= 4; ++test) {
+  for (int test = 1; test <= 5; ++test) {
     CK(cudaMemset(dO, 0, 128 * 128 * 4));
     switch (test) {
       case 1:
@@ -183,9 +198,13 @@ int main() {
         CK(cudaFuncSetAttribute(probe_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         probe_kernel<3><<<1, 128, smem>>>(m128A, m128B, dBs, dO);
         break;
-      default:
+      case 4:
         CK(cudaFuncSetAttribute(probe_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         probe_kernel<4><<<1, 128, smem>>>(m128A, m128B, dB, dO);
+        break;
+      default:
+        CK(cudaFuncSetAttribute(probe_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        probe_kernel<5><<<1, 128, smem>>>(m128A, m128B, dB, dO);
         break;
     }
     CK(cudaGetLastError());
@@ -201,7 +220,7 @@ int main() {
           if (test == 1) ref += bf(A[i * 128 + k]) * bf(Bs[j * 128 + k]);          // K[tok i] . Q[g j]
           else if (test == 2) ref += bf(A[k * 128 + i]) * bf(Bs[k * 16 + j]);     // V[tok k][d i] * P^T[k][g j]
           else if (test == 3) ref += bf(A[i * 128 + k]) * bf(B[j * 128 + k]);     // Q[i] . K[j]
-          else ref += bf(B[i * 128 + k]) * bf(A[k * 128 + j]);                    // P[i][k] * V[k][j]
+          else ref += bf(B[i * 128 + k]) * bf(A[k * 128 + j]);                    // P[i][k] * V[k][j] (T4, T5)
         }
         maxerr = fmax(maxerr, fabs(ref - O[i * N + j]));
         maxref = fmax(maxref, fabs(ref));
