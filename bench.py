@@ -293,15 +293,20 @@ def ev_ms(torch, stream, fn, iters=1):
 
 def prefill_rows(torch, dev_t, link, tf_peak):
     """a20 + a14 on config 2's 16k LayerKV request (7B, x=0: every layer
-    offloaded, reference min_retained_layers): per layer the causal prefill
-    attention on the tcgen05 kernel, then lkv_prefill_layer packs the layer's
-    K/V and streams it to the CPU slots' pinned frames on the D2H engine while
-    the next layer's attention runs. Reports the attention kernel against the
-    measured bf16 peak and how much of the offload the compute hides."""
+    offloaded, the reference's min_retained_layers at 16k). Per layer the
+    compute is the causal prefill attention on the tcgen05 kernel plus the
+    layer's dense GEMMs (QKV/O projections and the SwiGLU MLP of Llama-2-7B,
+    cuBLAS bf16 through torch.matmul: plain library GEMMs, random weights);
+    then lkv_prefill_layer packs the layer's K/V and streams it to the CPU
+    slots' pinned frames on the D2H engine while the next layer computes.
+    Reports the attention kernel against the measured bf16 peak, how much of
+    the offload the per-layer compute hides, and the measured prefill time
+    (TTFT of an idle server) beside the cost model's simulated one."""
     from paper_2410_00428_b200 import layersim as ls
     from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
     model = ls.llama2_7b()
     L, bs, d, T = model.n_layers, 16, model.d_head, 16384
+    hid, ffn = model.hidden, 11008
     nblk = T // bs
     kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model)
     # staging: 64 x 16 MiB, enough to absorb the D2H backlog of a prompt whose
@@ -316,21 +321,39 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     k = torch.empty((T, hl, d), dtype=torch.bfloat16, device=dev_t)
     v = torch.empty_like(k)
     out = torch.empty_like(q)
+    x = (torch.rand((T, hid), device=dev_t, generator=g) - 0.5).to(torch.bfloat16)
+    w_qkv = (torch.rand((hid, 3 * hid), device=dev_t, generator=g) - 0.5).to(torch.bfloat16) * 0.02
+    w_o = (torch.rand((hid, hid), device=dev_t, generator=g) - 0.5).to(torch.bfloat16) * 0.02
+    w_up = (torch.rand((hid, 2 * ffn), device=dev_t, generator=g) - 0.5).to(torch.bfloat16) * 0.02
+    w_dn = (torch.rand((ffn, hid), device=dev_t, generator=g) - 0.5).to(torch.bfloat16) * 0.02
     scale = 1.0 / math.sqrt(d)
     dev.fill_kv(k, v, T, 0, 0, SEED, stream=cs)
     attn = lambda: dev.prefill_attention(q, k, v, out, T, scale, DTYPE_BF16, stream=cs)  # noqa: E731
+
+    def dense():  # the layer's GEMMs (outputs discarded; same shapes and FLOPs as the model's)
+        with torch.cuda.stream(cs):
+            torch.matmul(x, w_qkv)
+            torch.matmul(out.view(T, hid), w_o)
+            u = torch.matmul(x, w_up)
+            torch.matmul(u[:, :ffn], w_dn)
+
+    def layer():
+        dense()
+        attn()
     attn()
+    dense()
     attn_ms = min(ev_ms(torch, cs, attn) for _ in range(3))
     flops = 4.0 * d * hq * T * (T + 1) / 2
-    # whole prompt: per layer attention + offload of the layer (compute-only run first)
-    compute_ms = ev_ms(torch, cs, lambda: [attn() for _ in range(L)])
+    # whole prompt: per-layer compute, then the same with the offload of every layer
+    compute_ms = ev_ms(torch, cs, lambda: [layer() for _ in range(L)])
     assert kv.allocate_prefill(0, T, 0)
 
     def prefill_with_offload():
-        for layer in range(L):
-            attn()
-            dev.prefill_layer(0, layer, k, v, T, stream=cs)
+        for layer_i in range(L):
+            layer()
+            dev.prefill_layer(0, layer_i, k, v, T, stream=cs)
         dev.synchronize()
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     prefill_with_offload()
     with_ms = (time.perf_counter() - t0) * 1e3
@@ -338,9 +361,11 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     bytes_off = ost.d2h_bytes_algorithmic
     link_ms = bytes_off / (link["d2h"] * 1e9) * 1e3
     exposed = max(0.0, with_ms - compute_ms)
-    # simulated TTFT of the same prefill (reference cost model, B200-like hardware spec)
+    # simulated prefill of the same prompt: reference cost model (Eq. 3,
+    # cost_model.cpp:39-44) with this box's measured bf16 peak and link
     hw = ls.HardwareSpec(tf_peak * 1e12, 6.55e12, link["d2h"] * 1e9, True, 1, 180e9, 0.9)
     sim = ls.prefill_time(model, hw, ls.CostParams(), T)
+    dense_flops = 2.0 * T * (hid * 3 * hid + hid * hid + hid * 2 * ffn + ffn * hid)
     dev.close()
     return {
         "a20_prefill_attention": {
@@ -348,13 +373,15 @@ def prefill_rows(torch, dev_t, link, tf_peak):
             "ms": attn_ms, "tflops": flops / attn_ms / 1e9, "peak_tflops": tf_peak,
             "frac": flops / attn_ms / 1e9 / tf_peak, "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)"},
         "a14_prefill_offload_overlap": {
-            "workload": f"1 request x {T} tokens, 7B, x=0 (all {L} layers offloaded): attention + pack + D2H per layer",
+            "workload": (f"1 request x {T} tokens, 7B, x=0 (all {L} layers offloaded); per layer: tcgen05 "
+                         f"attention + the layer's dense GEMMs (cuBLAS) on the compute stream, then pack + D2H"),
             "compute_only_ms": compute_ms, "with_offload_ms": with_ms, "exposed_offload_ms": exposed,
             "offload_bytes": bytes_off, "offload_alone_at_link_peak_ms": link_ms,
             "hidden_frac": max(0.0, 1.0 - exposed / link_ms) if link_ms else None,
             "offload_gbs_during_prefill": bytes_off / (with_ms / 1e3) / 1e9,
-            "measured_ttft_ms_attention_only": with_ms,
-            "simulated_prefill_s_cost_model": sim},
+            "layer_tflops": L * (flops + dense_flops) / compute_ms / 1e9,
+            "measured_prefill_ms": with_ms,
+            "simulated_prefill_ms_cost_model": sim * 1e3},
     }
 
 
@@ -565,7 +592,7 @@ def main():
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "decode_attn_v2_kernel<G=1>", "peak_kind": peak_kind,
                          "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms,
-                         "split_merge": {"kernel": "decode_merge_v3_kernel", "avg_launch_ms":
+                         "split_merge": {"kernel": "decode_merge_v4_kernel", "avg_launch_ms":
                                          merge_ms / max(attn_launches, 1),
                                          "attention_plus_merge_frac": per_launch_bytes / (
                                              (avg_launch_ms + merge_ms / max(attn_launches, 1)) / 1000) / 1e9 / hbm_peak}},

@@ -368,6 +368,49 @@ __global__ void __launch_bounds__(128) decode_merge_v3_kernel(const float* __res
                     out_f32, threadIdx.x & 31, g, G);
 }
 
+// Fused all-gather of the per-head outputs (the path's one
+// exchange). Every rank's gather buffer (cudaMalloc'd by its lkv_device,
+// opened by the peers through CUDA IPC) is
+//   [flags: kGatherFlagWords u32][rows: 2 parities x max_batch x Hq_total x 128 bf16]
+// The merge writes each final row into every rank's buffer at this rank's
+// head offset; the last CTA of the launch then raises flags[tp_rank] = epoch
+// in every buffer (release at system scope). A consumer waits for all flags.
+constexpr int kGatherFlagWords = 64;
+struct GatherArgs {
+  char* const* bases;   // device array [n] of gather buffer bases (peer pointers), or nullptr
+  int n;                // ranks
+  int rank;             // this rank = index of its own flag word
+  int hq_total;         // query heads over all ranks
+  int max_batch;
+  int parity;           // epoch & 1: row buffer of this layer
+  unsigned epoch;
+  unsigned* done;       // CTA completion counter (self re-arming)
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// A layer with no members still publishes its epoch.
+__global__ void gather_flag_kernel(GatherArgs ga) {
+  __threadfence_system();
+  for (int p = 0; p < ga.n; ++p) st_release_sys(reinterpret_cast<unsigned*>(ga.bases[p]) + ga.rank, ga.epoch);
+}
+
+// Waits until every rank raised its flag to `epoch` in this rank's buffer.
+__global__ void gather_wait_kernel(const unsigned* __restrict__ flags, int n, unsigned epoch) {
+  const int i = threadIdx.x;
+  if (i < n) {
+    while (static_cast<int>(ld_acquire_sys(flags + i) - epoch) < 0) __nanosleep(256);
+  }
+  __syncwarp();
+}
+
 // One CTA (4 warps) per (member, query head). Every warp finds the global max
 // over the chunks (lanes stride over chunks), then warp w folds chunks w,
 // w+4, ... with all its o-row loads issued before any FMA (8 in flight per
@@ -375,7 +418,8 @@ __global__ void __launch_bounds__(128) decode_merge_v3_kernel(const float* __res
 __global__ void __launch_bounds__(128) decode_merge_v4_kernel(const float* __restrict__ part_o,
                                                               const float* __restrict__ part_ml,
                                                               const AttnSeq* __restrict__ seqs, int Hl, int G,
-                                                              void* __restrict__ out, int out_f32) {
+                                                              void* __restrict__ out, int out_f32,
+                                                              GatherArgs ga) {
   __shared__ float4 so[4][32];
   __shared__ float sl[4];
   const int m = blockIdx.x, hq = blockIdx.y, h = hq / G, g = hq % G;
@@ -440,6 +484,30 @@ __global__ void __launch_bounds__(128) decode_merge_v4_kernel(const float* __res
       o[1] = __float2bfloat16_rn(r.y * inv);
       o[2] = __float2bfloat16_rn(r.z * inv);
       o[3] = __float2bfloat16_rn(r.w * inv);
+    }
+    if (ga.bases) {  // this row into every rank's gather buffer (NVLink stores to peers)
+      uint2 pk;
+      pk.x = (static_cast<unsigned>(__bfloat16_as_ushort(__float2bfloat16_rn(r.y * inv))) << 16) |
+             __bfloat16_as_ushort(__float2bfloat16_rn(r.x * inv));
+      pk.y = (static_cast<unsigned>(__bfloat16_as_ushort(__float2bfloat16_rn(r.w * inv))) << 16) |
+             __bfloat16_as_ushort(__float2bfloat16_rn(r.z * inv));
+      const long long row = (static_cast<long long>(ga.parity) * ga.max_batch + m) * ga.hq_total +
+                            static_cast<long long>(ga.rank) * Hl * G + hq;
+      const long long off = kGatherFlagWords * 4 + row * kHeadDim * 2 + lane * 8;
+      for (int p = 0; p < ga.n; ++p) *reinterpret_cast<uint2*>(ga.bases[p] + off) = pk;
+    }
+  }
+  if (ga.bases) {  // the launch's last CTA publishes the epoch to every rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned total = gridDim.x * gridDim.y;
+      if (atomicAdd(ga.done, 1u) == total - 1) {
+        __threadfence_system();
+        for (int p = 0; p < ga.n; ++p)
+          st_release_sys(reinterpret_cast<unsigned*>(ga.bases[p]) + ga.rank, ga.epoch);
+        *ga.done = 0u;
+      }
     }
   }
 }

@@ -134,6 +134,18 @@ struct lkv_device final : layersim::KvObserver {
   // bulk copies (decode_attn.cuh), 3 = tcgen05 GQA tile (decode_gqa_tc.cuh).
   // LKV_DECODE_KERNEL overrides the per-group-size default.
   int kernel_version = 2;
+  // ---- fused all-gather of per-head outputs (decode_attn.cuh GatherArgs)
+  char* d_gather = nullptr;                 // own gather buffer: flags | 2 parities of rows
+  std::size_t gather_bytes = 0;
+  std::vector<char*> gather_bases;          // per rank (own + IPC-opened or same-process peers)
+  std::vector<char*> gather_opened;         // IPC mappings to close
+  char** d_gather_bases = nullptr;
+  unsigned* d_gather_done = nullptr;
+  unsigned gather_epoch = 0;
+  std::vector<unsigned> layer_epoch;        // [L] epoch of the layer's last gather
+  bool gather_on() const { return d_gather_bases != nullptr; }
+  long long gather_rows_per_parity() const { return static_cast<long long>(cfg.max_batch) * Hql * cfg.tp_size; }
+
   int merge_version = 4;           // LKV_MERGE=2 / 3: earlier merge kernels (thread = dim / warp per head)
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
@@ -343,6 +355,10 @@ struct lkv_device final : layersim::KvObserver {
     cudaFree(d_aseqs);
     cudaFree(d_chunks);
     cudaFree(d_counter);
+    for (char* p : gather_opened) cudaIpcCloseMemHandle(p);
+    cudaFree(d_gather);
+    cudaFree(d_gather_bases);
+    cudaFree(d_gather_done);
     for (auto s : {cs, d2h, h2d})
       if (s) cudaStreamDestroy(s);
   }
@@ -939,6 +955,46 @@ struct lkv_device final : layersim::KvObserver {
     join_out(user);
   }
 
+  // Gather arguments of layer l's merge: a fresh epoch per decode_layer call
+  // (every rank makes the same calls, so epochs agree across ranks).
+  GatherArgs gather_args(int l) {
+    GatherArgs ga{};
+    if (!gather_on()) return ga;
+    ++gather_epoch;
+    layer_epoch[l] = gather_epoch;
+    ga.bases = d_gather_bases;
+    ga.n = cfg.tp_size;
+    ga.rank = cfg.tp_rank;
+    ga.hq_total = Hql * cfg.tp_size;
+    ga.max_batch = cfg.max_batch;
+    ga.parity = static_cast<int>(gather_epoch & 1u);
+    ga.epoch = gather_epoch;
+    ga.done = d_gather_done;
+    return ga;
+  }
+
+  char* gather_buffer() {
+    if (!d_gather) {
+      gather_bytes = kGatherFlagWords * 4 + 2ull * gather_rows_per_parity() * D * 2;
+      LKV_CUDA(cudaMalloc(&d_gather, gather_bytes));
+      LKV_CUDA(cudaMemsetAsync(d_gather, 0, gather_bytes, cs));
+      LKV_CUDA(cudaStreamSynchronize(cs));
+    }
+    return d_gather;
+  }
+
+  void gather_connect(const std::vector<char*>& bases) {
+    if (static_cast<int>(bases.size()) != cfg.tp_size) throw std::invalid_argument("gather: need one base per rank");
+    if (cfg.tp_size > kGatherFlagWords) throw std::invalid_argument("gather: too many ranks");
+    if (bases[cfg.tp_rank] != gather_buffer()) throw std::invalid_argument("gather: own slot must be own buffer");
+    gather_bases = bases;
+    if (!d_gather_bases) LKV_CUDA(cudaMalloc(&d_gather_bases, kGatherFlagWords * sizeof(char*)));
+    if (!d_gather_done) LKV_CUDA(cudaMalloc(&d_gather_done, sizeof(unsigned)));
+    LKV_CUDA(cudaMemcpy(d_gather_bases, bases.data(), bases.size() * sizeof(char*), cudaMemcpyHostToDevice));
+    LKV_CUDA(cudaMemset(d_gather_done, 0, sizeof(unsigned)));
+    layer_epoch.assign(L, 0);
+  }
+
   void decode_layer(int l, const void* q, void* out, float scale, int f32, cudaStream_t user) {
     if (!in_iteration) throw layersim::SimulationError("decode_layer outside decode_begin/end");
     check_layer(l);
@@ -973,16 +1029,19 @@ struct lkv_device final : layersim::KvObserver {
       }
       if (timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attention kernel | merge kernel
       // merge (members without KV get zero rows: no chunks, L = 0)
+      if (gather_on() && merge_version != 4) throw std::invalid_argument("fused gather needs merge v4");
       if (merge_version == 2)
         decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
       else if (merge_version == 3)
         decode_merge_v3_kernel<<<(n * Hql + 3) / 4, 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, n, Hl, G, out, f32);
       else
-        decode_merge_v4_kernel<<<dim3(n, Hql), 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
+        decode_merge_v4_kernel<<<dim3(n, Hql), 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32,
+                                                             gather_args(l));
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;
       dstats.kernel_launches += n_chunks > 0 ? 2 : 1;
     } else if (n > 0) {
+      if (gather_on()) throw std::invalid_argument("fused gather needs decode kernel v2/v3");
       const int pairs = n * Hl;
       const int target = 4 * sms;
       int n_split = std::max(1, std::min((target + pairs - 1) / pairs, std::max(max_nblk, 1)));
@@ -1009,6 +1068,11 @@ struct lkv_device final : layersim::KvObserver {
         decode_merge_kernel<<<n * Hql, D, 0, cs>>>(d_part_o, d_part_ml, n_split, D, out, f32);
         LKV_CUDA(cudaGetLastError());
       }
+    }
+    if (n == 0 && gather_on()) {  // nothing to send, but peers still wait for this epoch
+      const GatherArgs ga = gather_args(l);
+      gather_flag_kernel<<<1, 1, 0, cs>>>(ga);
+      LKV_CUDA(cudaGetLastError());
     }
     if (timing) LKV_CUDA(cudaEventRecord(t_attn1[l], cs));
     LKV_CUDA(cudaEventRecord(attn_done[st], cs));
@@ -1191,6 +1255,69 @@ int lkv_decode_layer(lkv_device* d, int32_t layer, const void* q, void* out, flo
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
   d->decode_layer(layer, q, out, scale, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<cudaStream_t>(stream));
   LKV_CATCH
+}
+
+int lkv_device_gather_buffer(lkv_device* d, void** base, uint64_t* bytes) {
+  LKV_REQUIRE(d && base && bytes);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  *base = d->gather_buffer();
+  *bytes = d->gather_bytes;
+  LKV_CATCH
+}
+
+int lkv_device_gather_ipc_handle(lkv_device* d, void* handle) {
+  LKV_REQUIRE(d && handle);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  cudaIpcMemHandle_t h;
+  LKV_CUDA(cudaIpcGetMemHandle(&h, d->gather_buffer()));
+  std::memcpy(handle, &h, sizeof h);
+  LKV_CATCH
+}
+
+int lkv_device_gather_connect_ipc(lkv_device* d, const void* handles, int32_t n) {
+  LKV_REQUIRE(d && handles && n == d->cfg.tp_size);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  std::vector<char*> bases(n);
+  for (int r = 0; r < n; ++r) {
+    if (r == d->cfg.tp_rank) {
+      bases[r] = d->gather_buffer();
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + r * sizeof h, sizeof h);
+    void* p = nullptr;
+    LKV_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+    d->gather_opened.push_back(static_cast<char*>(p));
+    bases[r] = static_cast<char*>(p);
+  }
+  d->gather_connect(bases);
+  LKV_CATCH
+}
+
+int lkv_device_gather_connect(lkv_device* d, void* const* bases, int32_t n) {
+  LKV_REQUIRE(d && bases && n == d->cfg.tp_size);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  std::vector<char*> b(n);
+  for (int r = 0; r < n; ++r) b[r] = static_cast<char*>(bases[r]);
+  d->gather_connect(b);
+  LKV_CATCH
+}
+
+int lkv_decode_gather_wait(lkv_device* d, int32_t layer, void* stream) {
+  LKV_REQUIRE(d && d->gather_on() && layer >= 0 && layer < d->L);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->cs;
+  gather_wait_kernel<<<1, 32, 0, s>>>(reinterpret_cast<const unsigned*>(d->d_gather), d->cfg.tp_size,
+                                      d->layer_epoch[layer]);
+  LKV_CUDA(cudaGetLastError());
+  LKV_CATCH
+}
+
+int lkv_decode_gathered(lkv_device* d, int32_t layer, void** rows) {
+  LKV_REQUIRE(d && d->gather_on() && rows && layer >= 0 && layer < d->L);
+  const long long parity = d->layer_epoch[layer] & 1u;
+  *rows = d->d_gather + kGatherFlagWords * 4 + parity * d->gather_rows_per_parity() * d->D * 2;
+  return LKV_OK;
 }
 
 int lkv_decode_end(lkv_device* d) {

@@ -83,9 +83,11 @@ for cap in ("prefill_attn", "decode_gqa_tc"):
                           capture_output=True, text=True).stdout
     ops = collections.Counter()
     for ln in sass.splitlines():
-        for m in ("UTCHMMA", "UTCBAR", "UTMALDG", "UBLKCP", "LDTM", "STTM", "MUFU.EX2", "HMMA"):
+        for m in ("UTCHMMA", "UTCBAR", "UTMALDG", "UBLKCP", "LDTM", "STTM", "MUFU.EX2"):
             if m in ln:
                 ops[m] += 1
+        if "HMMA" in ln.replace("UTCHMMA", ""):  # legacy mma.sync path (must stay 0)
+            ops["HMMA(legacy)"] += 1
     lines.append("# SASS opcodes present (static count in the source page): " +
                  ", ".join(f"{k}={v}" for k, v in sorted(ops.items())))
     with open(os.path.join(out_dir, f"{tag}_{cap}_ncu.txt"), "w") as f:
