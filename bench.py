@@ -61,6 +61,9 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-rows", action="store_true", help="skip the tensor-core / overlap rows beside the headline")
+    p.add_argument("--allgather", default="fused", choices=["fused", "nccl"],
+                   help="N>1 exchange of per-head outputs: fused into the merge kernel over NVLink peer memory "
+                        "(product) or a separate NCCL all-gather (baseline)")
     return p.parse_args()
 
 
@@ -253,7 +256,10 @@ def workload_config(args):
             "model_shape": "llama2-7b", "batch": args.batch, "context": args.ctx, "retained_layers": args.retained,
             "kv_residency": "pinned host frames (CPU slots), prefetched per layer",
             "l2": "inputs larger than L2 (one layer's KV = 1.88 GB)",
-            "parallelism": f"kv-head tp{args.gpus}", "pipeline_depth": args.depth}
+            "parallelism": f"kv-head tp{args.gpus}", "pipeline_depth": args.depth,
+            "allgather": (None if args.gpus == 1 else
+                          "fused into decode_merge_v4_kernel (NVLink peer stores + epoch flags)" if args.allgather == "fused"
+                          else "NCCL all_gather_into_tensor")}
 
 
 def simulated_ttft(ctx):
@@ -438,10 +444,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("LKV_BENCH_ONE_GPU") == "1":  # code-path check only: every rank on cuda:0 (numbers meaningless)
+        local = 0
     torch.cuda.set_device(local)
     dev_t = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev_t)
+        # control plane (handle exchange, barriers, max over ranks) on gloo; NCCL only for the baseline all-gather
+        if args.allgather == "nccl":
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev_t)
+        else:
+            dist.init_process_group("gloo")
     from paper_2410_00428_b200 import layersim as ls
     from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
 
@@ -486,8 +498,14 @@ def main():
     scale = 1.0 / math.sqrt(d)
     q = [torch.randn((B, hql, d), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
     out = [torch.empty((B, hql, d), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
+    fused = world > 1 and args.allgather == "fused"
     gathered = [torch.empty((world * B * hql * d,), dtype=torch.bfloat16, device=dev_t) for _ in range(L)] \
-        if world > 1 else None
+        if world > 1 and not fused else None
+    if fused:  # exchange gather-buffer IPC handles once; the merge kernel then stores into every rank's buffer
+        handles = [None] * world
+        dist.all_gather_object(handles, dev.gather_ipc_handle())
+        dev.gather_connect_ipc(handles)
+        dist.barrier()
     dev.set_timing(True)
 
     def step(qsrc=None, outdst=None):
@@ -497,8 +515,10 @@ def main():
                 with torch.cuda.stream(cs):
                     q[layer].copy_(qsrc[layer], non_blocking=True)
             dev.decode_layer(layer, q[layer], out[layer], scale, DTYPE_BF16, stream=cs)
-            if world > 1:
-                with torch.cuda.stream(cs):  # the one collective: all-gather of per-head outputs
+            if fused:  # the one exchange, done by the merge kernel: wait for every rank's rows of this layer
+                dev.gather_wait(layer, stream=cs)
+            elif world > 1:
+                with torch.cuda.stream(cs):  # baseline: a separate NCCL all-gather of per-head outputs
                     dist.all_gather_into_tensor(gathered[layer], out[layer].reshape(-1))
             if outdst is not None:
                 with torch.cuda.stream(cs):
@@ -523,7 +543,7 @@ def main():
             attn_ms += st.attn_ms
             merge_ms += st.merge_ms
             h2d_ms += st.h2d_ms
-            launches += st.kernel_launches
+            launches += st.kernel_launches + (L if fused else 0)  # + the per-layer gather_wait_kernel
             attn_launches += st.attn_launches
             h2d_alg += st.h2d_bytes_algorithmic
             h2d_phys += st.h2d_bytes_physical
@@ -533,7 +553,7 @@ def main():
         torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1)
     if world > 1:
-        t = torch.tensor([elapsed], device=dev_t)
+        t = torch.tensor([elapsed], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         elapsed = float(t.item())
         dist.barrier()
@@ -553,7 +573,7 @@ def main():
         dev.synchronize()
     e2e_s = time.perf_counter() - t0
     if world > 1:
-        t = torch.tensor([e2e_s], device=dev_t, dtype=torch.float64)
+        t = torch.tensor([e2e_s], dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
     e2e_value = total_kv * args.steps / e2e_s / 1e9

@@ -295,6 +295,37 @@ LKV_API int lkv_decode_layer(lkv_device* dev, int32_t layer, const void* q, void
                              int32_t out_dtype, void* stream);
 LKV_API int lkv_decode_end(lkv_device* dev);
 
+/* ---- fused all-gather of per-head decode outputs ----------
+ * The path's one exchange: after each layer's decode attention every rank
+ * needs every rank's per-head rows (the reference models it as the per-layer
+ * all-reduce window of cost_model.cpp:81-88 / interconnect.cpp:57-61, zero on
+ * NVLink). Instead of a separate collective, the split-merge kernel of
+ * lkv_decode_layer stores each finished row straight into every rank's
+ * gather buffer over NVLink (peer pointers) and its last CTA raises this
+ * rank's epoch flag in every buffer. Rows of layer l land at
+ *   gathered[l] = [max_batch][q_heads_local * tp_size][head_dim] bf16
+ * (rank r's heads at column block r), double-buffered by layer parity: the
+ * caller must consume gathered(l) (after lkv_decode_gather_wait) before its
+ * next-but-one lkv_decode_layer.
+ * Setup (once, before the first decode): each rank exports a handle, the
+ * handles are exchanged out of band (e.g. torch.distributed all_gather), and
+ * each rank connects with all tp_size handles in rank order. */
+#define LKV_IPC_HANDLE_BYTES 64
+LKV_API int lkv_device_gather_ipc_handle(lkv_device* dev, void* handle /* LKV_IPC_HANDLE_BYTES */);
+LKV_API int lkv_device_gather_connect_ipc(lkv_device* dev, const void* handles /* tp_size * 64 B */,
+                                          int32_t tp_size);
+/* Same-process ranks (several devices in one process, or tests that put
+ * every rank on one GPU): connect with the raw device pointers of each
+ * rank's lkv_device_gather_buffer. */
+LKV_API int lkv_device_gather_buffer(lkv_device* dev, void** base, uint64_t* bytes);
+LKV_API int lkv_device_gather_connect(lkv_device* dev, void* const* bases, int32_t tp_size);
+/* Enqueue on `stream` (NULL = compute stream) a wait until every rank has
+ * published `layer`'s rows of the current iteration; afterwards *rows of
+ * lkv_decode_gathered is readable on that stream. A rank missing for 20 s
+ * traps the kernel (the context fails loudly instead of hanging). */
+LKV_API int lkv_decode_gather_wait(lkv_device* dev, int32_t layer, void* stream);
+LKV_API int lkv_decode_gathered(lkv_device* dev, int32_t layer, void** rows);
+
 /* Serving decode with KV write-back. Like lkv_decode_begin,
  * but the iteration also appends each member's new token at position
  * cached_tokens (the block append_decode_block provided, engine.cpp:408-409)

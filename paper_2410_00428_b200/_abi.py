@@ -16,6 +16,7 @@ LIB_PATH = os.path.join(_HERE, "liblkv.so")
 i32, i64, u8, u32, u64, f64, f32 = C.c_int32, C.c_int64, C.c_uint8, C.c_uint32, C.c_uint64, C.c_double, C.c_float
 P = C.POINTER
 vp = C.c_void_p
+IPC_HANDLE_BYTES = 64  # LKV_IPC_HANDLE_BYTES (cudaIpcMemHandle_t)
 
 
 class ModelSpec(C.Structure):
@@ -160,6 +161,12 @@ _PROTOS = {
     "lkv_decode_begin_append": [vp, P(i64), i32],
     "lkv_decode_append_layer": [vp, i32, vp, vp, vp],
     "lkv_decode_end": [vp],
+    "lkv_device_gather_ipc_handle": [vp, vp],
+    "lkv_device_gather_connect_ipc": [vp, vp, i32],
+    "lkv_device_gather_buffer": [vp, P(vp), P(u64)],
+    "lkv_device_gather_connect": [vp, P(vp), i32],
+    "lkv_decode_gather_wait": [vp, i32, vp],
+    "lkv_decode_gathered": [vp, i32, P(vp)],
     "lkv_device_set_timing": [vp, i32],
     "lkv_decode_last_stats": [vp, P(DecodeStats)],
     "lkv_offload_last_stats": [vp, P(OffloadStats), i32],
@@ -171,7 +178,7 @@ _RET = {"lkv_last_error": C.c_char_p, "lkv_version": C.c_char_p}
 
 DEVICE_SYMBOLS = [n for n in _PROTOS if n.startswith(("lkv_device", "lkv_prefill_layer", "lkv_prefill_attention", "lkv_decode_begin",
                                                      "lkv_decode_layer", "lkv_decode_end", "lkv_decode_last",
-                                                     "lkv_decode_append",
+                                                     "lkv_decode_append", "lkv_decode_gather",
                                                      "lkv_offload_last", "lkv_fill", "lkv_verify"))]
 ALL_SYMBOLS = list(_PROTOS) + list(_RET)
 

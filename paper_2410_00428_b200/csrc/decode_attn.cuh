@@ -406,7 +406,14 @@ __global__ void gather_flag_kernel(GatherArgs ga) {
 __global__ void gather_wait_kernel(const unsigned* __restrict__ flags, int n, unsigned epoch) {
   const int i = threadIdx.x;
   if (i < n) {
-    while (static_cast<int>(ld_acquire_sys(flags + i) - epoch) < 0) __nanosleep(256);
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (static_cast<int>(ld_acquire_sys(flags + i) - epoch) < 0) {
+      __nanosleep(256);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (t - t0 > 20000000000ull) __trap();  // a rank never published: fail loudly, do not hang
+    }
   }
   __syncwarp();
 }

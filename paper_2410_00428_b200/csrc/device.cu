@@ -1265,6 +1265,8 @@ int lkv_device_gather_buffer(lkv_device* d, void** base, uint64_t* bytes) {
   LKV_CATCH
 }
 
+static_assert(sizeof(cudaIpcMemHandle_t) == LKV_IPC_HANDLE_BYTES, "lkv.h LKV_IPC_HANDLE_BYTES");
+
 int lkv_device_gather_ipc_handle(lkv_device* d, void* handle) {
   LKV_REQUIRE(d && handle);
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));

@@ -52,6 +52,17 @@ def _stream(stream):
     return C.c_void_p(stream.cuda_stream)
 
 
+def _device_view(ptr: int, shape, dtype, device: int):
+    """A torch tensor aliasing device memory owned by liblkv (no copy)."""
+    import torch
+
+    class _Arr:
+        __cuda_array_interface__ = {"shape": tuple(shape), "typestr": "<i2", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    with torch.cuda.device(device):
+        return torch.as_tensor(_Arr(), device=torch.device("cuda", device)).view(dtype)
+
+
 class Device:
     """One GPU's KV-head shard of the LayerKV data path, bound to a KvManager."""
 
@@ -138,6 +149,43 @@ class Device:
 
     def decode_end(self):
         self._lib.call("lkv_decode_end", self.handle)
+
+    # ------------------------------------------------------------- fused all-gather
+    def gather_ipc_handle(self) -> bytes:
+        """This rank's gather-buffer IPC handle, to exchange out of band."""
+        buf = C.create_string_buffer(_abi.IPC_HANDLE_BYTES)
+        self._lib.call("lkv_device_gather_ipc_handle", self.handle, buf)
+        return buf.raw
+
+    def gather_connect_ipc(self, handles):
+        """Connect with every rank's handle (rank order, own included)."""
+        blob = b"".join(handles)
+        if len(blob) != _abi.IPC_HANDLE_BYTES * len(handles):
+            raise ValueError("gather handles must be 64 bytes each")
+        self._lib.call("lkv_device_gather_connect_ipc", self.handle, blob, len(handles))
+
+    def gather_buffer(self) -> int:
+        base, n = C.c_void_p(), C.c_uint64()
+        self._lib.call("lkv_device_gather_buffer", self.handle, C.byref(base), C.byref(n))
+        return base.value
+
+    def gather_connect(self, bases):
+        """Same-process ranks: connect with each rank's gather_buffer() pointer."""
+        arr = (C.c_void_p * len(bases))(*bases)
+        self._lib.call("lkv_device_gather_connect", self.handle, arr, len(bases))
+
+    def gather_wait(self, layer: int, stream=None):
+        """Enqueue on `stream` a wait for every rank's rows of `layer`."""
+        self._lib.call("lkv_decode_gather_wait", self.handle, layer, _stream(stream))
+
+    def gathered(self, layer: int):
+        """torch view [max_batch, q_heads_local * tp_size, head_dim] bf16 of
+        layer's gathered rows (valid on a stream after gather_wait)."""
+        import torch
+        p = C.c_void_p()
+        self._lib.call("lkv_decode_gathered", self.handle, layer, C.byref(p))
+        shape = (self.cfg.max_batch, self.q_heads_local * self.cfg.tp_size, self.head_dim)
+        return _device_view(p.value, shape, torch.bfloat16, self.cfg.device)
 
     def decode_stats(self) -> _abi.DecodeStats:
         s = _abi.DecodeStats()
