@@ -374,6 +374,11 @@ LKV_API int lkv_offload_last_stats(const lkv_device* dev, lkv_offload_stats* out
  * [tokens][kv_heads_local][head_dim] K and V for tokens [token0, token0+tokens). */
 LKV_API int lkv_fill_kv(lkv_device* dev, void* k, void* v, int64_t tokens, int64_t token0, int32_t layer,
                 uint64_t seed, void* stream);
+/* Generator K/V of one token per row: row m (of n) is token positions[m]
+ * (host array) of layer `layer`, [n][kv_heads_local][head_dim] bf16 — the
+ * new tokens of a decode step in tests and the serving loop. */
+LKV_API int lkv_fill_kv_tokens(lkv_device* dev, void* k, void* v, const int64_t* positions, int32_t n,
+                               int32_t layer, uint64_t seed, void* stream);
 /* Counts 4-byte words of the request's KV (every layer, tokens < n_tokens) that
  * differ from the generator, wherever they live now: GPU slots, or pinned
  * host frames read directly by the kernel. */
@@ -382,6 +387,88 @@ LKV_API int lkv_verify_request(lkv_device* dev, int64_t request_id, int64_t n_to
 /* Writes generator data for every entry of a request (GPU slots and host
  * frames) without going through prefill — bench setup only. */
 LKV_API int lkv_fill_request(lkv_device* dev, int64_t request_id, int64_t n_tokens, uint64_t seed);
+
+/* ======================================================================== *
+ * Serving loop and trace / CSV formats (f4).
+ * The reference's caller of the path — engine.cpp's event loop with the
+ * SLO-aware scheduler (scheduler.cpp), its traces (workload.cpp) and
+ * requests.csv (metrics.cpp:91-101) — restated over this library. The
+ * executor decides where time comes from:
+ *   MODELLED         cost model + serial PcieBus: byte-identical requests.csv
+ *                    to the reference (no GPU needed);
+ *   DEVICE_VIRTUAL   the GPU executes every prefill / escalation / decode
+ *                    iteration through the data path, the clock stays
+ *                    modelled (so the schedule, and requests.csv, are the
+ *                    reference's) — parity mode with real bytes;
+ *   DEVICE_MEASURED  the GPU executes and CUDA events give the times:
+ *                    measured TTFT / TPOT under the same scheduler.
+ * ======================================================================== */
+#define LKV_SERVE_MODELLED 0
+#define LKV_SERVE_DEVICE_VIRTUAL 1
+#define LKV_SERVE_DEVICE_MEASURED 2
+
+typedef struct lkv_serve_config { /* reference EngineConfig, engine.hpp:32-50 */
+  lkv_model_spec model;
+  lkv_hardware_spec hw;
+  lkv_cost_params cost;
+  double ttft_slo, tpot_slo;
+  int32_t policy_layerkv, slo_scheduler;
+  int64_t gpu_blocks, cpu_blocks;
+  int32_t tokens_per_block, horizon;
+  double threshold_fraction, predictor_accuracy;
+  int64_t max_batch_tokens;
+  double max_time, chunk_bytes;
+  uint64_t seed;
+  int32_t force_retained_layers, invariant_checks;
+  /* device executor */
+  int32_t executor;          /* LKV_SERVE_* */
+  int32_t device;            /* CUDA ordinal */
+  int32_t dense_gemms;       /* per-layer QKV/O/MLP GEMMs (cuBLAS) in prefill and decode */
+  int32_t prefill_attention; /* tcgen05 causal attention per prefill layer */
+  int32_t verify_kv;         /* check each request's KV bit-exact vs the generator before release */
+  int32_t pipeline_depth;    /* decode prefetch depth (layers) */
+  int64_t ffn;               /* MLP width of the dense GEMMs; 0 = derived from n_param */
+  int64_t host_slots;        /* pinned host frames; 0 = cpu_blocks */
+  uint64_t kv_seed;          /* generator seed of the synthetic K/V */
+} lkv_serve_config;
+
+typedef struct lkv_serve_summary { /* MetricsReport (metrics.hpp) + transfer totals + device stats */
+  double mean_ttft, p50_ttft, p99_ttft, mean_tpot, throughput, makespan;
+  int64_t d2h_jobs, h2d_jobs;
+  double d2h_bytes, h2d_bytes;
+  int32_t completed, n_rows;
+  int32_t violations, pad_;
+  int64_t prefills, decode_iterations, kv_words_mismatched, requests_verified, gpu_kernel_launches;
+  double prefill_device_s, decode_device_s;
+  int64_t escalations; /* offload jobs planned by the escalation path */
+} lkv_serve_summary;
+
+typedef struct lkv_serve_request_row { /* one requests.csv row (metrics.hpp RequestMetrics) */
+  int64_t id;
+  double arrival, queuing, prefill, ttft, mean_tpot;
+  int32_t output_tokens, violated;
+} lkv_serve_request_row;
+
+/* Runs the trace (arrays of n requests, ascending arrival) to completion.
+ * rows (may be NULL) receives min(rows_cap, n_rows) rows in id order. */
+LKV_API int lkv_serve_run(const lkv_serve_config* cfg, int32_t n, const int64_t* ids, const double* arrival,
+                          const int32_t* prompt, const int32_t* output, lkv_serve_summary* out,
+                          lkv_serve_request_row* rows, int32_t rows_cap);
+/* requests.csv text of rows (metrics.cpp:91-101): *len = bytes (no NUL),
+ * written when cap > *len. */
+LKV_API int lkv_serve_requests_csv(const lkv_serve_request_row* rows, int32_t n, char* buf, size_t cap,
+                                   size_t* len);
+/* generate_fixed / generate_sharegpt_like (workload.cpp:35-82), n requests. */
+LKV_API int lkv_trace_generate(int32_t sharegpt, int32_t n, int32_t prompt, int32_t output, double rate,
+                               uint64_t seed, int64_t* ids, double* arrival, int32_t* prompt_out,
+                               int32_t* output_out);
+/* load_trace (workload.cpp:84-136): *n = records; arrays (may be NULL to
+ * size) receive min(cap, *n); *unsorted = 1 when input was re-sorted. */
+LKV_API int lkv_trace_read_jsonl(const char* path, int64_t* ids, double* arrival, int32_t* prompt,
+                                 int32_t* output, int32_t cap, int32_t* n, int32_t* unsorted);
+/* save_trace (workload.cpp:138-148). */
+LKV_API int lkv_trace_write_jsonl(const char* path, int32_t n, const int64_t* ids, const double* arrival,
+                                  const int32_t* prompt, const int32_t* output);
 
 #ifdef __cplusplus
 }

@@ -384,4 +384,29 @@ LKV_API int ref_generate_trace(int32_t kind_sharegpt, int32_t n, int32_t prompt,
   CATCH
 }
 
+// Reference load_trace / save_trace (workload.cpp:84-148): JSONL format parity.
+// Returns the record count (arrays filled up to cap), or -1 on error.
+LKV_API int ref_load_trace(const char* path, int64_t* ids, double* arrival, int32_t* p, int32_t* o, int32_t cap) {
+  try {
+    Trace t = load_trace(path);
+    for (std::size_t i = 0; i < t.requests.size() && static_cast<int32_t>(i) < cap; ++i) {
+      ids[i] = t.requests[i].id;
+      arrival[i] = t.requests[i].arrival;
+      p[i] = t.requests[i].prompt_tokens;
+      o[i] = t.requests[i].output_tokens;
+    }
+    return static_cast<int>(t.requests.size());
+  } catch (...) {
+    return -1;
+  }
+}
+
+LKV_API int ref_save_trace(const char* path, int32_t n, const int64_t* ids, const double* arrival, const int32_t* p,
+                           const int32_t* o) {
+  TRY Trace t;
+  for (int32_t i = 0; i < n; ++i) t.requests.push_back({ids[i], arrival[i], p[i], o[i]});
+  save_trace(t, path);
+  CATCH
+}
+
 }  // extern "C"

@@ -75,6 +75,29 @@ class SpanC(C.Structure):
     _fields_ = [("begin", f64), ("end", f64), ("is_allreduce", i32), ("pad_", i32)]
 
 
+class ServeConfigC(C.Structure):
+    _fields_ = [("model", ModelSpec), ("hw", HardwareSpec), ("cost", CostParams), ("ttft_slo", f64),
+                ("tpot_slo", f64), ("policy_layerkv", i32), ("slo_scheduler", i32), ("gpu_blocks", i64),
+                ("cpu_blocks", i64), ("tokens_per_block", i32), ("horizon", i32), ("threshold_fraction", f64),
+                ("predictor_accuracy", f64), ("max_batch_tokens", i64), ("max_time", f64), ("chunk_bytes", f64),
+                ("seed", u64), ("force_retained_layers", i32), ("invariant_checks", i32), ("executor", i32),
+                ("device", i32), ("dense_gemms", i32), ("prefill_attention", i32), ("verify_kv", i32),
+                ("pipeline_depth", i32), ("ffn", i64), ("host_slots", i64), ("kv_seed", u64)]
+
+
+class ServeSummaryC(C.Structure):
+    _fields_ = [("mean_ttft", f64), ("p50_ttft", f64), ("p99_ttft", f64), ("mean_tpot", f64), ("throughput", f64),
+                ("makespan", f64), ("d2h_jobs", i64), ("h2d_jobs", i64), ("d2h_bytes", f64), ("h2d_bytes", f64),
+                ("completed", i32), ("n_rows", i32), ("violations", i32), ("pad_", i32), ("prefills", i64),
+                ("decode_iterations", i64), ("kv_words_mismatched", i64), ("requests_verified", i64),
+                ("gpu_kernel_launches", i64), ("prefill_device_s", f64), ("decode_device_s", f64), ("escalations", i64)]
+
+
+class ServeRowC(C.Structure):
+    _fields_ = [("id", i64), ("arrival", f64), ("queuing", f64), ("prefill", f64), ("ttft", f64),
+                ("mean_tpot", f64), ("output_tokens", i32), ("violated", i32)]
+
+
 class DeviceConfig(C.Structure):
     _fields_ = [("device", i32), ("tp_rank", i32), ("tp_size", i32), ("pipeline_depth", i32),
                 ("gpu_slots", i64), ("host_slots", i64), ("arena_slots", i64),
@@ -171,6 +194,13 @@ _PROTOS = {
     "lkv_decode_last_stats": [vp, P(DecodeStats)],
     "lkv_offload_last_stats": [vp, P(OffloadStats), i32],
     "lkv_fill_kv": [vp, vp, vp, i64, i64, i32, u64, vp],
+    "lkv_fill_kv_tokens": [vp, vp, vp, P(i64), i32, i32, u64, vp],
+    # serving loop and trace formats
+    "lkv_serve_run": [P(ServeConfigC), i32, P(i64), P(f64), P(i32), P(i32), P(ServeSummaryC), P(ServeRowC), i32],
+    "lkv_serve_requests_csv": [P(ServeRowC), i32, C.c_char_p, C.c_size_t, P(C.c_size_t)],
+    "lkv_trace_generate": [i32, i32, i32, i32, f64, u64, P(i64), P(f64), P(i32), P(i32)],
+    "lkv_trace_read_jsonl": [C.c_char_p, P(i64), P(f64), P(i32), P(i32), i32, P(i32), P(i32)],
+    "lkv_trace_write_jsonl": [C.c_char_p, i32, P(i64), P(f64), P(i32), P(i32)],
     "lkv_verify_request": [vp, i64, i64, u64, P(i64)],
     "lkv_fill_request": [vp, i64, i64, u64],
 }
@@ -179,7 +209,8 @@ _RET = {"lkv_last_error": C.c_char_p, "lkv_version": C.c_char_p}
 DEVICE_SYMBOLS = [n for n in _PROTOS if n.startswith(("lkv_device", "lkv_prefill_layer", "lkv_prefill_attention", "lkv_decode_begin",
                                                      "lkv_decode_layer", "lkv_decode_end", "lkv_decode_last",
                                                      "lkv_decode_append", "lkv_decode_gather",
-                                                     "lkv_offload_last", "lkv_fill", "lkv_verify"))]
+                                                     "lkv_offload_last", "lkv_fill", "lkv_verify",
+                                                     "lkv_serve", "lkv_trace"))]
 ALL_SYMBOLS = list(_PROTOS) + list(_RET)
 
 

@@ -562,7 +562,7 @@ struct lkv_device final : layersim::KvObserver {
       d2h_segment(seg, cpu.data(), cnt);
     }
     cudaEvent_t ev;
-    ev_create(&ev);
+    ev_create(&ev, true);
     LKV_CUDA(cudaEventRecord(ev, d2h));
     job_ev[job.job_id] = ev;
     ostats.jobs += 1;
@@ -1107,6 +1107,22 @@ struct lkv_device final : layersim::KvObserver {
     }                                             \
   } while (0)
 
+namespace lkv {
+void device_bind_manager(lkv_device* d, KvManager& k) {
+  if (k.n_layers() != d->L) throw std::invalid_argument("bind: layer count mismatch");
+  if (k.tokens_per_block() != d->bs) throw std::invalid_argument("bind: tokens_per_block mismatch");
+  if (!k.request_ids().empty()) throw std::invalid_argument("bind: manager already holds requests");
+  d->kv = &k;
+  k.set_observer(d);
+}
+// Completion event of an escalation job's last D2H copy (timing-capable);
+// null once complete_offload consumed it.
+cudaEvent_t device_job_event(lkv_device* d, std::int64_t job_id) {
+  auto it = d->job_ev.find(job_id);
+  return it == d->job_ev.end() ? nullptr : it->second;
+}
+}  // namespace lkv
+
 extern "C" {
 
 int lkv_device_create(const lkv_model_spec* m, int32_t tpb, const lkv_device_config* c,
@@ -1145,14 +1161,10 @@ int lkv_device_get_info(const lkv_device* d, lkv_device_info* o) {
   return LKV_OK;
 }
 
+
 int lkv_device_bind(lkv_device* d, lkv_kv_manager* kv) {
   LKV_REQUIRE(d && kv);
-  LKV_TRY KvManager& k = lkv::kv_impl(kv);
-  if (k.n_layers() != d->L) throw std::invalid_argument("bind: layer count mismatch");
-  if (k.tokens_per_block() != d->bs) throw std::invalid_argument("bind: tokens_per_block mismatch");
-  if (!k.request_ids().empty()) throw std::invalid_argument("bind: manager already holds requests");
-  d->kv = &k;
-  k.set_observer(d);
+  LKV_TRY lkv::device_bind_manager(d, lkv::kv_impl(kv));
   LKV_CATCH
 }
 
@@ -1385,6 +1397,24 @@ int lkv_fill_kv(lkv_device* d, void* k, void* v, int64_t tokens, int64_t token0,
     fill_kv_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v),
                                         tokens, token0, layer, d->Hl, d->head0, d->D, seed);
     LKV_CUDA(cudaGetLastError());
+  }
+  LKV_CATCH
+}
+
+int lkv_fill_kv_tokens(lkv_device* d, void* k, void* v, const int64_t* positions, int32_t n, int32_t layer,
+                       uint64_t seed, void* stream) {
+  LKV_REQUIRE(d && k && v && (positions || n == 0) && n >= 0);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->cs;
+  if (n > 0) {
+    auto* pos = reinterpret_cast<long long*>(d->ring.reserve(n * sizeof(long long)));
+    std::memcpy(pos, positions, n * sizeof(long long));
+    const long long total = static_cast<long long>(n) * d->Hl * d->D;
+    const int grid = static_cast<int>(std::min<long long>((total + 255) / 256, 8ll * d->sms));
+    fill_kv_tokens_kernel<<<grid, 256, 0, s>>>(static_cast<__nv_bfloat16*>(k), static_cast<__nv_bfloat16*>(v), pos,
+                                               n, layer, d->Hl, d->head0, d->D, seed);
+    LKV_CUDA(cudaGetLastError());
+    d->ring.commit(s);
   }
   LKV_CATCH
 }

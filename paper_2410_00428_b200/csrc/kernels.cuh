@@ -419,6 +419,22 @@ __global__ void fill_kv_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat16* __r
   }
 }
 
+// Generator K/V of one token per row: row m holds token pos[m] of its own
+// request (the decode step's new tokens).
+__global__ void fill_kv_tokens_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat16* __restrict__ v,
+                                      const long long* __restrict__ pos, int n, int layer, int Hl, int head0,
+                                      int D, unsigned long long seed) {
+  const long long total = static_cast<long long>(n) * Hl * D;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int d = static_cast<int>(i % D);
+    const int h = static_cast<int>((i / D) % Hl);
+    const long long t = pos[i / (static_cast<long long>(D) * Hl)];
+    reinterpret_cast<unsigned short*>(k)[i] = kv_value_bf16(seed, layer, 0, t, head0 + h, d);
+    reinterpret_cast<unsigned short*>(v)[i] = kv_value_bf16(seed, layer, 1, t, head0 + h, d);
+  }
+}
+
 // One CTA per (block, layer) of a request: compare (or write) every element
 // of the slot against the generator. The slot is found through the table
 // mirror: GPU slot -> device pool, ~cpu_slot -> pinned host pool (read or

@@ -21,5 +21,7 @@ void set_error(const std::string& msg);
 int status_from_current_exception();
 layersim::ModelSpec to_model(const lkv_model_spec* m);
 layersim::KvManager& kv_impl(lkv_kv_manager* kv);
+// device.cu: bind a device to a manager owned elsewhere (the serving loop).
+void device_bind_manager(lkv_device* d, layersim::KvManager& k);
 
 }  // namespace lkv

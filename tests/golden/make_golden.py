@@ -41,6 +41,9 @@ ENGINE_SCENARIOS = {
                             trace=("list", [(0, 0.0, 512, 64), (1, 0.1, 768, 8), (2, 0.2, 16, 8)])),
     "te_slo_ablation": dict(model="llama2_7b", pools=(200000, 800000), layerkv=True, slo=False, force=-1, seed=7,
                             trace=("fixed", 60, 4096, 64, 2.0, 29)),
+    # small escalation case for the device-executed serving loop (3 Half/Full escalations)
+    "esc_small": dict(model="llama2_7b", pools=(600, 20000), layerkv=True, force=-1, seed=3, invariant=True,
+                      trace=("sharegpt", 12, 20.0, 17)),
     # 70B GQA, TP8 over NVLink, half retained (config 4 shape, 4k + 64)
     "cfg4_tp8": dict(model="llama31_70b_gqa", tp=8, nvlink=True, pools=(2000000, 16000000), layerkv=True, force=40,
                      trace=("single", 4096, 65)),

@@ -13,7 +13,7 @@ from tests.golden import make_golden as mg
 FAST = ["cfg1_x32", "cfg1_x16", "cfg1_x0", "cfg2_baseline_128", "cfg2_layerkv_128", "cfg2_baseline_1024",
         "cfg2_layerkv_1024", "cfg2_baseline_2048", "cfg2_layerkv_2048", "te_determinism_layerkv",
         "te_determinism_baseline", "te_contended", "te_fcfs_layerkv", "cfg4_tp8", "cfg2_baseline_4096",
-        "cfg2_layerkv_4096", "te_slo_ablation", "cfg2_baseline_16384", "cfg2_layerkv_16384"]
+        "cfg2_layerkv_4096", "te_slo_ablation", "cfg2_baseline_16384", "cfg2_layerkv_16384", "esc_small"]
 
 
 def _run(lib, name):

@@ -1,0 +1,131 @@
+"""Serving loop and trace / CSV formats (f4).
+
+The product's own loop (paper_2410_00428_b200/csrc/serve_engine.cpp) with the
+modelled executor must reproduce the REFERENCE engine's requests.csv byte for
+byte and its summary numbers exactly, on every BASELINE.json trace
+(tests/golden/engine.json, written by the compiled reference). The traces
+come from the product's restated generators, so the same hashes also pin
+generate_fixed / generate_sharegpt_like. Where the reference is built here,
+the generators and JSONL I/O are compared with it directly."""
+from __future__ import annotations
+
+import hashlib
+import json
+import os
+
+import pytest
+
+from paper_2410_00428_b200 import layersim as ls
+from paper_2410_00428_b200 import serve
+from tests import _drivers as drv
+from tests.golden import make_golden as mg
+from tests.test_engine_dropin import FAST
+
+SUMMARY_KEYS = ["mean_ttft", "p50_ttft", "p99_ttft", "mean_tpot", "throughput", "makespan", "d2h_jobs", "h2d_jobs",
+                "d2h_bytes", "h2d_bytes", "completed", "n_rows"]
+
+
+def product_trace(spec) -> serve.Trace:
+    kind = spec[0]
+    if kind == "single":
+        return serve.Trace([0], [0.0], [spec[1]], [spec[2]])
+    if kind == "fixed":
+        _, n, p, o, rate, seed = spec
+        return serve.generate_fixed(n, p, o, rate, seed)
+    if kind == "sharegpt":
+        _, n, rate, seed = spec
+        return serve.generate_sharegpt_like(n, rate, seed)
+    rows = spec[1]
+    return serve.Trace([r[0] for r in rows], [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows])
+
+
+def serve_cfg(sc, **kw) -> serve.ServeConfig:
+    hw = ls.default_hardware()
+    hw.n_gpus = sc.get("tp", 1)
+    hw.nvlink = sc.get("nvlink", False)
+    return serve.ServeConfig(model=getattr(ls, sc["model"])(), hw=hw, layerkv=sc["layerkv"],
+                             slo_scheduler=sc.get("slo", True), gpu_blocks=sc["pools"][0], cpu_blocks=sc["pools"][1],
+                             seed=sc.get("seed", 0), force_retained_layers=sc["force"],
+                             invariant_checks=sc.get("invariant", False), **kw)
+
+
+@pytest.fixture(scope="module")
+def engine_golden():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "engine.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", FAST)
+def test_serve_loop_matches_reference_golden(engine_golden, name):
+    sc = mg.ENGINE_SCENARIOS[name]
+    summary, rows, csv = serve.run(serve_cfg(sc), product_trace(sc["trace"]))
+    g = engine_golden[name]
+    assert csv.splitlines()[:3] == g["csv_head"]
+    assert hashlib.sha256(csv.encode()).hexdigest() == g["csv_sha256"]
+    assert {k: summary[k] for k in SUMMARY_KEYS} == g["summary"]
+
+
+def test_trace_generators_match_reference(ref):
+    for sharegpt, args in ((False, (100, 16384, 512, 1.0, 1)), (False, (7, 3, 9, 0.25, 123)),
+                           (True, (150, 0, 0, 6.0, 11)), (True, (500, 0, 0, 10.0, 17))):
+        want = drv.generate_trace(ref, sharegpt, *args)
+        got = serve._generate(sharegpt, *args, None)
+        assert (got.ids, got.arrival, got.prompt, got.output) == tuple(list(x) for x in want)
+
+
+def test_jsonl_round_trip_and_errors(tmp_path):
+    t = serve.generate_sharegpt_like(40, 3.0, 5)
+    p = tmp_path / "t.jsonl"
+    serve.save_trace(t, p)
+    back, unsorted = serve.load_trace(p)
+    assert not unsorted and back == t  # shortest round-trip doubles: exact
+    first = p.read_text().splitlines()[0]
+    rec = json.loads(first)
+    assert set(rec) == {"id", "arrival_s", "prompt_tokens", "output_tokens"}
+
+    q = tmp_path / "u.jsonl"
+    q.write_text('# comment\n{"arrival_s": 2.5, "prompt_tokens": 10, "output_tokens": 3}\n\n'
+                 '  {"output_tokens": 1, "prompt_tokens": 4, "arrival_s": 1}\n')
+    back, unsorted = serve.load_trace(q)
+    assert unsorted and back.ids == [1, 0] and back.arrival == [1.0, 2.5] and back.prompt == [4, 10]
+
+    for body, msg in (('{"arrival_s": 1, "prompt_tokens": 2}\n', "missing field 'output_tokens'"),
+                      ('{"arrival_s": 1, "prompt_tokens": 2, "output_tokens": 0}\n', "invariant violation"),
+                      ('{"arrival_s": 1, "prompt_tokens": 2\n', "parse error"),
+                      ('# only a comment\n', "contains no records")):
+        bad = tmp_path / "bad.jsonl"
+        bad.write_text(body)
+        with pytest.raises(ls.LkvError, match=msg):
+            serve.load_trace(bad)
+    with pytest.raises(ls.LkvError, match="bad.jsonl:1"):
+        bad.write_text('{"arrival_s": "x", "prompt_tokens": 2, "output_tokens": 1}\n')
+        serve.load_trace(bad)
+
+
+def test_reference_reads_product_jsonl(ref, tmp_path):
+    """The reference's own load_trace (nlohmann json) reads what the product
+    writes, and vice versa, to the same requests."""
+    if not hasattr(ref.dll, "ref_load_trace"):
+        pytest.skip("reference shim has no ref_load_trace")
+    import ctypes as C
+    t = serve.generate_sharegpt_like(25, 2.0, 9)
+    p = tmp_path / "p.jsonl"
+    serve.save_trace(t, p)
+    n = len(t)
+    ids, arr, pr, o = (C.c_int64 * n)(), (C.c_double * n)(), (C.c_int32 * n)(), (C.c_int32 * n)()
+    assert ref.dll.ref_load_trace(str(p).encode(), ids, arr, pr, o, n) == n
+    assert (list(ids), list(arr), list(pr), list(o)) == (t.ids, t.arrival, t.prompt, t.output)
+    q = tmp_path / "r.jsonl"
+    assert ref.dll.ref_save_trace(str(q).encode(), n, ids, arr, pr, o) == 0
+    back, _ = serve.load_trace(q)
+    assert back == t
+
+
+def test_errors_are_loud():
+    sc = mg.ENGINE_SCENARIOS["te_fcfs_layerkv"]
+    cfg = serve_cfg(sc)
+    cfg.gpu_blocks, cfg.cpu_blocks = 8, 8  # the 512-token head can never fit
+    with pytest.raises(ls.SimulationError, match="can never be admitted"):
+        serve.run(cfg, product_trace(sc["trace"]))
+    with pytest.raises(ls.LkvError, match="arrivals not sorted"):
+        serve.run(serve_cfg(sc), serve.Trace([0, 1], [1.0, 0.5], [4, 4], [2, 2]))
