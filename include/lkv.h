@@ -291,6 +291,9 @@ LKV_API int lkv_decode_begin(lkv_device* dev, const int64_t* request_ids, int32_
  * after the work already queued on it, and its later work sees `out`. */
 #define LKV_DTYPE_BF16 0
 #define LKV_DTYPE_F32 1
+/* Stream arguments of the device half: NULL = the device's compute stream
+ * (no ordering with any caller stream); pass cudaStreamLegacy ((void*)1) to
+ * order with CUDA's legacy default stream (e.g. torch's default stream). */
 LKV_API int lkv_decode_layer(lkv_device* dev, int32_t layer, const void* q, void* out, float scale,
                              int32_t out_dtype, void* stream);
 LKV_API int lkv_decode_end(lkv_device* dev);

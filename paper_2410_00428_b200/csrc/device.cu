@@ -146,6 +146,11 @@ struct lkv_device final : layersim::KvObserver {
   bool gather_on() const { return d_gather_bases != nullptr; }
   long long gather_rows_per_parity() const { return static_cast<long long>(cfg.max_batch) * Hql * cfg.tp_size; }
 
+  // fp16 copy of a prefill layer's V for the PF16 attention path
+  void* d_vh = nullptr;
+  std::size_t vh_cap = 0;
+  cudaEvent_t vh_free = nullptr;
+  bool vh_used = false;
   int merge_version = 4;           // LKV_MERGE=2 / 3: earlier merge kernels (thread = dim / warp per head)
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
@@ -315,6 +320,7 @@ struct lkv_device final : layersim::KvObserver {
     ev_create(&t_pack0, true);
     ev_create(&t_pack1, true);
     ev_create(&ev_join);
+    ev_create(&vh_free);
     for (int r = cfg.max_requests - 1; r >= 0; --r) free_rows.push_back(r);
   }
 
@@ -355,6 +361,8 @@ struct lkv_device final : layersim::KvObserver {
     cudaFree(d_aseqs);
     cudaFree(d_chunks);
     cudaFree(d_counter);
+    cudaFree(d_vh);
+    if (vh_free) cudaEventDestroy(vh_free);
     for (char* p : gather_opened) cudaIpcCloseMemHandle(p);
     cudaFree(d_gather);
     cudaFree(d_gather_bases);
@@ -1194,23 +1202,51 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   if (tokens > 0x7FFFFF80ll) throw std::invalid_argument("prefill_attention: too many tokens");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->cs;
   const uint64_t T = static_cast<uint64_t>(tokens), D = static_cast<uint64_t>(d->D);
+  // LKV_PREFILL_P=bf16x2: P as bf16 hi + lo against bf16 V (two PV MMAs);
+  // default fp16 P against an fp16 copy of V (one PV MMA).
+  static const bool pf16 = [] {
+    const char* e = std::getenv("LKV_PREFILL_P");
+    return !(e && std::strcmp(e, "bf16x2") == 0);
+  }();
+  const void* vsrc = v;
+  if (pf16) {  // fp16 copy of V in a device scratch (bf16 -> fp16 is exact in fp16's normal range)
+    const std::size_t need = static_cast<std::size_t>(T) * d->Hl * D * 2;
+    if (need > d->vh_cap) {
+      LKV_CUDA(cudaDeviceSynchronize());
+      cudaFree(d->d_vh);
+      LKV_CUDA(cudaMalloc(&d->d_vh, need));
+      d->vh_cap = need;
+    }
+    if (d->vh_used) LKV_CUDA(cudaStreamWaitEvent(s, d->vh_free, 0));  // previous user of the scratch
+    const long long n8 = static_cast<long long>(need / 16);
+    const int grid = static_cast<int>(std::min<long long>((n8 + 255) / 256, 8ll * d->sms));
+    bf16_to_f16_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(v), static_cast<uint4*>(d->d_vh), n8);
+    LKV_CUDA(cudaGetLastError());
+    vsrc = d->d_vh;
+  }
   CUtensorMap qm, km, vm;
   if (!tc::make_map_3d(&qm, q, D, d->Hql, T, D * 2, D * 2 * d->Hql, 64, 1, 128, true) ||
       !tc::make_map_3d(&km, k, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true) ||
-      !tc::make_map_3d(&vm, v, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true))
+      !tc::make_map_3d(&vm, vsrc, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true,
+                       pf16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
     throw CudaError("prefill_attention: cuTensorMapEncodeTiled failed (pointers must be 16 B aligned)");
   // LKV_PREFILL_WG=1: one softmax warpgroup per CTA (thread = whole row); default 2 (row split in halves)
   static const int nwg = [] {
     const char* e = std::getenv("LKV_PREFILL_WG");
     return (e && std::atoi(e) == 1) ? 1 : 2;
   }();
-  auto fn = nwg == 1 ? prefill_attn_kernel<1> : prefill_attn_kernel<2>;
+  auto fn = nwg == 1 ? (pf16 ? prefill_attn_kernel<1, true> : prefill_attn_kernel<1, false>)
+                     : (pf16 ? prefill_attn_kernel<2, true> : prefill_attn_kernel<2, false>);
   d->smem_attr(reinterpret_cast<const void*>(fn), PrefillAttnSmem::kBytes);
   const dim3 grid(static_cast<unsigned>((tokens + 127) / 128), static_cast<unsigned>(d->Hql));
   fn<<<grid, 96 + 128 * nwg, PrefillAttnSmem::kBytes, s>>>(
       qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
       scale * 1.4426950408889634f);
   LKV_CUDA(cudaGetLastError());
+  if (pf16) {
+    LKV_CUDA(cudaEventRecord(d->vh_free, s));
+    d->vh_used = true;
+  }
   LKV_CATCH
 }
 

@@ -9,6 +9,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -416,6 +417,22 @@ __global__ void fill_kv_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat16* __r
     const unsigned short vb = kv_value_bf16(seed, layer, 1, token0 + t, head0 + h, d);
     reinterpret_cast<unsigned short*>(k)[i] = kb;
     reinterpret_cast<unsigned short*>(v)[i] = vb;
+  }
+}
+
+// bf16 -> fp16, 8 values per thread step (the PF16 prefill attention's V
+// copy). Exact for |x| in fp16's normal range [2^-14, 65504].
+__global__ void bf16_to_f16_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, long long n8) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
+    const uint4 a = __ldcs(src + i);
+    const uint32_t w[4] = {a.x, a.y, a.z, a.w};
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const __half2 h = __floats2half2_rn(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u));
+      o[j] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    dst[i] = make_uint4(o[0], o[1], o[2], o[3]);
   }
 }
 

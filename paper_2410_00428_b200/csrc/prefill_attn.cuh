@@ -21,16 +21,20 @@
 //              column half), its 128/NWG columns of the row in registers.
 //              Lazy rescaling: the running max only moves when a tile
 //              exceeds it by more than 2^8; only then does the warp wait for
-//              the previous PV and rescale its O columns in TMEM. P = hi + lo
-//              in bf16 (two MMAs into the same O): 2^-15 relative, inside the
-//              1e-3 parity bar; the split is integer AND/PRMT so the XU pipe
-//              only runs ex2.
+//              the previous PV and rescale its O columns in TMEM.
+//              P precision (bf16 P alone misses the 1e-3 bar: 2^-9 per
+//              weight). PF16 (default): P in fp16 (2^-11) against an fp16
+//              copy of V made by lkv_prefill_attention (every bf16 value in
+//              fp16's normal range converts exactly), one PV MMA per tile.
+//              !PF16: P = hi + lo in bf16, two MMAs into the same O (2^-15,
+//              1.5x the MMA work); the split is integer AND/PRMT.
 // TMEM: S0/P0 [0,128) S1/P1 [128,256) O [256,384) of a 512-column allocation;
 // P of tile j sits in S(j)'s columns: hi [0,64), lo [64,128), two bf16 per
 // column (K = token pairs), 8 columns per K=16 MMA step.
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -66,7 +70,7 @@ __device__ __forceinline__ void prefill_named_bar(int id, int n) {
 // NWG softmax warpgroups split each S row by columns (NWG=2: two threads per
 // query row, 64 columns each), doubling the softmax issue rate per SM; the
 // halves exchange row maxima through smem once per tile.
-template <int NWG>
+template <int NWG, bool PF16>
 __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
@@ -149,7 +153,7 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
-      constexpr uint32_t idO = tc::idesc_bf16(128, 128, false, true);
+      constexpr uint32_t idO = PF16 ? tc::idesc_f16(128, 128, false, true) : tc::idesc_bf16(128, 128, false, true);
       const uint32_t q0 = tc::saddr(sm + S::kQ), k0 = tc::saddr(sm + S::kK), v0 = tc::saddr(sm + S::kV);
       // PV(i) reads P(i) from S(i)'s TMEM columns; it is issued before
       // S(i+2) (same columns), and tcgen05.mma executes in issue order.
@@ -164,7 +168,7 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
         for (int kk = 0; kk < 8; ++kk) {
           const uint64_t bd = tc::smem_desc(vt + kk * 2048, 16384, 1024, tc::kLayoutSw128);
           tc::mma_bf16_ts(tmem + 256, pt + kk * 8, bd, idO, (i > 0 || kk > 0));
-          tc::mma_bf16_ts(tmem + 256, pt + 64 + kk * 8, bd, idO, 1u);
+          if constexpr (!PF16) tc::mma_bf16_ts(tmem + 256, pt + 64 + kk * 8, bd, idO, 1u);
         }
         tc::mma_commit(o_full);
         tc::mma_commit(&v_empty[vs]);
@@ -262,18 +266,28 @@ __global__ void __launch_bounds__(96 + 128 * NWG, 1) prefill_attn_kernel(
       // written (in-order tensor pipe).
 #pragma unroll
       for (int c = 0; c < CPT / 32; ++c) {
-        uint32_t hi[16], lo[16];
-#pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float a = s[c * 32 + 2 * i], b = s[c * 32 + 2 * i + 1];
-          const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
-          const float ra = a - __uint_as_float(ua & 0xFFFF0000u), rb = b - __uint_as_float(ub & 0xFFFF0000u);
-          hi[i] = __byte_perm(ua, ub, 0x7632);
-          lo[i] = __byte_perm(__float_as_uint(ra), __float_as_uint(rb), 0x7632);
-        }
         const uint32_t col = sb * 128 + c0 / 2 + c * 16;
-        tc::tmem_st16(tl + col, hi);
-        tc::tmem_st16(tl + col + 64, lo);
+        if constexpr (PF16) {  // one fp16 P (2^-11 relative) against the fp16 copy of V
+          uint32_t ph[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const __half2 h2 = __floats2half2_rn(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]);
+            ph[i] = *reinterpret_cast<const uint32_t*>(&h2);
+          }
+          tc::tmem_st16(tl + col, ph);
+        } else {
+          uint32_t hi[16], lo[16];
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float a = s[c * 32 + 2 * i], b = s[c * 32 + 2 * i + 1];
+            const uint32_t ua = __float_as_uint(a), ub = __float_as_uint(b);
+            const float ra = a - __uint_as_float(ua & 0xFFFF0000u), rb = b - __uint_as_float(ub & 0xFFFF0000u);
+            hi[i] = __byte_perm(ua, ub, 0x7632);
+            lo[i] = __byte_perm(__float_as_uint(ra), __float_as_uint(rb), 0x7632);
+          }
+          tc::tmem_st16(tl + col, hi);
+          tc::tmem_st16(tl + col + 64, lo);
+        }
       }
       tc::tmem_wait_st();
       tc::fence_before_sync();

@@ -40,16 +40,25 @@ def _ptr(t) -> int:
     return t.data_ptr() if hasattr(t, "data_ptr") else int(t)
 
 
+_CUDA_STREAM_LEGACY = 1  # cudaStreamLegacy: CUDA's legacy default stream, torch's default stream
+
+
 def _stream(stream):
     """Caller's stream handle: the given torch stream, else torch's current
-    stream on the current device (so tensors produced there are ordered)."""
+    stream on the current device (so tensors produced there are ordered).
+    torch's default stream is CUDA's legacy stream 0; it is passed as
+    cudaStreamLegacy, because a NULL handle means "the device's compute
+    stream" in the C ABI — passing 0 would drop the ordering with the
+    caller's tensors (the non-blocking compute stream does not synchronise
+    with stream 0), and the caching allocator could recycle an input (e.g.
+    a freed q) before the kernel reads it."""
     if stream is None:
         try:
             import torch
             stream = torch.cuda.current_stream()
         except Exception:
             return None
-    return C.c_void_p(stream.cuda_stream)
+    return C.c_void_p(stream.cuda_stream or _CUDA_STREAM_LEGACY)
 
 
 def _device_view(ptr: int, shape, dtype, device: int):

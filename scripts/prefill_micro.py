@@ -43,7 +43,7 @@ def main():
     for it in range(a.iters + 2):
         torch.cuda.synchronize()
         e0.record(s)
-        dev.prefill_attention(q, k, v, out, T, 1 / math.sqrt(128), DTYPE_BF16)
+        dev.prefill_attention(q, k, v, out, T, 1 / math.sqrt(128), DTYPE_BF16, stream=s)
         e1.record(s)
         e1.synchronize()
         if it >= 2:

@@ -5,9 +5,11 @@
 //   T3  S[128x128]   = Q (K-major SW128, TMA) . K^T (K-major SW128, TMA)
 //   T4  O[128x128]   = P (K-major SW128, st.shared) . V (MN-major SW128, TMA)
 //   T5  O[128x128]   = P (TMEM, tcgen05.st; TS form) . V (MN-major SW128, TMA)
+//   T6  as T5 with P in fp16 and V in bf16 (mixed A/B formats of kind::f16)
 // Build: nvcc -std=c++17 -O2 -gencode arch=compute_100a,code=sm_100a -I paper_2410_00428_b200/csrc
 //        scripts/tc_probe.cu -o build/tc_probe
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <cmath>
 #include <cstdio>
@@ -88,7 +90,7 @@ __global__ void __launch_bounds__(128, 1)
       *reinterpret_cast<__nv_bfloat16*>(s.b + (t / 8) * 256 + (g / 8) * 128 + (t % 8) * 16 + (g % 8) * 2) =
           bsrc[i];
     }
-  } else if (TEST == 5) {
+  } else if (TEST == 5 || TEST == 6) {
     // P [128 q][128 tok] -> TMEM columns [128, 192): lane = row, two bf16 per column
     const uint32_t lane_addr = tmem + (static_cast<uint32_t>(warp * 32) << 16) + 128;
     for (int c = 0; c < 4; ++c) {
@@ -134,7 +136,8 @@ __global__ void __launch_bounds__(128, 1)
         bd = smem_desc(b0 + kk * 2048, 16384, 1024, kLayoutSw128);
         id = idesc_bf16(128, 128, false, true);
       }
-      if (TEST == 5)
+      if (TEST == 6) id = (id & ~(7u << 7));  // a_format = F16 (0), b_format stays BF16
+      if (TEST == 5 || TEST == 6)
         mma_bf16_ts(tmem, tmem + 128 + kk * 8, bd, id, kk > 0);
       else
         mma_bf16(tmem, ad, bd, id, kk > 0);
@@ -183,7 +186,12 @@ int main() {
   }
   const size_t smem = sizeof(Smem) + 1024;
   int fails = 0;
-  for (int test = 1; test <= 5; ++test) {
+  std::vector<__half> Bh(128 * 128);
+  for (size_t i = 0; i < B.size(); ++i) Bh[i] = __float2half(__bfloat162float(B[i]) * 0.999f);
+  __half* dBh;
+  CK(cudaMalloc(&dBh, Bh.size() * 2));
+  CK(cudaMemcpy(dBh, Bh.data(), Bh.size() * 2, cudaMemcpyHostToDevice));
+  for (int test = 1; test <= 6; ++test) {
     CK(cudaMemset(dO, 0, 128 * 128 * 4));
     switch (test) {
       case 1:
@@ -202,9 +210,13 @@ int main() {
         CK(cudaFuncSetAttribute(probe_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         probe_kernel<4><<<1, 128, smem>>>(m128A, m128B, dB, dO);
         break;
-      default:
+      case 5:
         CK(cudaFuncSetAttribute(probe_kernel<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
         probe_kernel<5><<<1, 128, smem>>>(m128A, m128B, dB, dO);
+        break;
+      default:
+        CK(cudaFuncSetAttribute(probe_kernel<6>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        probe_kernel<6><<<1, 128, smem>>>(m128A, m128B, reinterpret_cast<const __nv_bfloat16*>(dBh), dO);
         break;
     }
     CK(cudaGetLastError());
@@ -220,6 +232,7 @@ int main() {
           if (test == 1) ref += bf(A[i * 128 + k]) * bf(Bs[j * 128 + k]);          // K[tok i] . Q[g j]
           else if (test == 2) ref += bf(A[k * 128 + i]) * bf(Bs[k * 16 + j]);     // V[tok k][d i] * P^T[k][g j]
           else if (test == 3) ref += bf(A[i * 128 + k]) * bf(B[j * 128 + k]);     // Q[i] . K[j]
+          else if (test == 6) ref += __half2float(Bh[i * 128 + k]) * bf(A[k * 128 + j]);  // fp16 P * bf16 V
           else ref += bf(B[i * 128 + k]) * bf(A[k * 128 + j]);                    // P[i][k] * V[k][j] (T4, T5)
         }
         maxerr = fmax(maxerr, fabs(ref - O[i * N + j]));

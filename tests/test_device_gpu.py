@@ -176,3 +176,35 @@ def test_capacity_error_is_loud():
     kv, dev = sc.make(model, gpu=64, cpu=64)
     with pytest.raises(ls.CapacityError):
         dev.decode_begin(list(range(9)))  # > max_batch
+
+
+def test_default_stream_inputs_are_ordered():
+    """decode_layer with the caller on torch's default (legacy) stream: the
+    caller's next write to q must wait until the attention read it (the
+    regression: a NULL handle dropped the join, and a recycled q buffer was
+    overwritten before layer 0's kernel ran)."""
+    import math
+
+    import numpy as np
+    import torch
+    import oracle
+    from paper_2410_00428_b200.device import DTYPE_F32
+    model = sc.gqa_model(L=1, hkv=8, group=1)
+    kv, dev = sc.make(model, gpu=2000, cpu=2000, max_blocks=1300, arena=2000)
+    n_tok = 20000  # offloaded: the attention waits for a 20k-token prefetch first
+    sc.prefill(kv, dev, 0, n_tok, 0)
+    q_host = sc.random_q(1, 8, 128, 99)
+    q = q_host.to("cuda:0")
+    out = torch.empty((1, 8, 128), dtype=torch.float32, device="cuda:0")
+    dev.decode_begin([0])
+    dev.decode_layer(0, q, out, 1 / math.sqrt(128), DTYPE_F32)  # stream=None: torch's current (default) stream
+    q.fill_(7.0)  # default stream: must run after the kernel consumed q
+    dev.decode_end()
+    dev.synchronize()
+    torch.cuda.synchronize()
+    re = oracle.restatement()
+    want = re.decode_attn_gen(sc.SEED, 0, n_tok, 0, 8, 1, q_host.view(torch.int16).numpy().view(np.uint16)[0],
+                              1 / math.sqrt(128))
+    got = out[0].cpu().numpy()
+    err = np.abs(got - want).max(axis=-1) / np.abs(want).max(axis=-1)
+    assert err.max() <= sc.REL_TOL
