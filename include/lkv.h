@@ -228,6 +228,12 @@ typedef struct lkv_device_config {
   int32_t max_batch;      /* decode batch members */
   int32_t staging_chunks; /* D2H staging ring segments */
   int64_t chunk_bytes;    /* D2H staging segment size (reference TransferJob.chunk_bytes) */
+  /* Tiered host memory. 0: host_slots
+   * pinned frames, frame = CPU slot. > 0: every CPU slot's home is pageable
+   * (host_slots of them, one MAP_NORESERVE mapping) and this many pinned,
+   * device-mapped frames carry the DMA and in-kernel accesses; a cleaner
+   * thread writes dirty frames home, missing slots are read in on demand. */
+  int64_t pinned_frames;
 } lkv_device_config;
 
 typedef struct lkv_device_info {
@@ -387,6 +393,13 @@ LKV_API int lkv_fill_kv_tokens(lkv_device* dev, void* k, void* v, const int64_t*
  * host frames read directly by the kernel. */
 LKV_API int lkv_verify_request(lkv_device* dev, int64_t request_id, int64_t n_tokens, uint64_t seed,
                        int64_t* mismatches);
+/* One CPU slot's bytes (slot_bytes) into dst, wherever they live (pinned
+ * frame or pageable home); waits for in-flight copies into it. */
+LKV_API int lkv_device_read_host_slot(lkv_device* dev, int64_t cpu_slot, void* dst);
+typedef struct lkv_host_tier_stats {
+  int64_t pinned_frames, read_in_frames, write_back_frames, evictions, hits, misses;
+} lkv_host_tier_stats;
+LKV_API int lkv_device_host_tier_stats(const lkv_device* dev, lkv_host_tier_stats* out);
 /* Writes generator data for every entry of a request (GPU slots and host
  * frames) without going through prefill — bench setup only. */
 LKV_API int lkv_fill_request(lkv_device* dev, int64_t request_id, int64_t n_tokens, uint64_t seed);

@@ -102,7 +102,12 @@ class DeviceConfig(C.Structure):
     _fields_ = [("device", i32), ("tp_rank", i32), ("tp_size", i32), ("pipeline_depth", i32),
                 ("gpu_slots", i64), ("host_slots", i64), ("arena_slots", i64),
                 ("max_requests", i32), ("max_blocks", i32), ("max_batch", i32),
-                ("staging_chunks", i32), ("chunk_bytes", i64)]
+                ("staging_chunks", i32), ("chunk_bytes", i64), ("pinned_frames", i64)]
+
+
+class HostTierStats(C.Structure):
+    _fields_ = [("pinned_frames", i64), ("read_in_frames", i64), ("write_back_frames", i64), ("evictions", i64),
+                ("hits", i64), ("misses", i64)]
 
 
 class DeviceInfo(C.Structure):
@@ -203,6 +208,8 @@ _PROTOS = {
     "lkv_trace_write_jsonl": [C.c_char_p, i32, P(i64), P(f64), P(i32), P(i32)],
     "lkv_verify_request": [vp, i64, i64, u64, P(i64)],
     "lkv_fill_request": [vp, i64, i64, u64],
+    "lkv_device_read_host_slot": [vp, i64, vp],
+    "lkv_device_host_tier_stats": [vp, P(HostTierStats)],
 }
 _RET = {"lkv_last_error": C.c_char_p, "lkv_version": C.c_char_p}
 

@@ -53,6 +53,9 @@ int status_from_current_exception() {
   } catch (const std::invalid_argument& e) {
     g_error = e.what();
     return LKV_ERR_INVALID;
+  } catch (const std::length_error& e) {  // a bounded arena (e.g. pinned host frames) is exhausted
+    g_error = e.what();
+    return LKV_ERR_CAPACITY;
   } catch (const std::exception& e) {
     g_error = e.what();
     return LKV_ERR_INTERNAL;

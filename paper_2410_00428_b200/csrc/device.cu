@@ -26,6 +26,7 @@
 #include "decode_attn.cuh"
 #include "decode_gqa_tc.cuh"
 #include "prefill_attn.cuh"
+#include "host_tier.hpp"
 #include "kernels.cuh"
 #include "layersim/errors.hpp"
 #include "layersim/kv_manager.hpp"
@@ -120,7 +121,28 @@ struct lkv_device final : layersim::KvObserver {
 
   // ---- memory
   char* dbuf = nullptr;        // pool | arena stages
-  char* host_pool = nullptr;   // pinned, CPU slot frames
+  char* host_pool = nullptr;   // pinned, CPU slot frames (tiered: the pinned frame tier)
+  // ---- tiered host memory: pageable homes + pinned frames
+  HostTier tier;
+  int* d_xlat = nullptr;        // [host_slots] CPU slot -> pinned frame (verify/fill kernels)
+  bool tiered() const { return tier.enabled(); }
+  // Frames of CPU slots for device access (identity when not tiered);
+  // host_done() must follow once the work using them is enqueued on `st`.
+  void host_frames(const std::vector<long long>& slots, bool read, std::vector<long long>* frames) {
+    frames->resize(slots.size());
+    if (!tiered()) {
+      std::copy(slots.begin(), slots.end(), frames->begin());
+      return;
+    }
+    if (!slots.empty()) tier.pin(slots.data(), static_cast<long long>(slots.size()), read, frames->data());
+  }
+  void host_done(const std::vector<long long>& slots, cudaStream_t st, bool write) {
+    if (!tiered() || slots.empty()) return;
+    cudaEvent_t ev;
+    ev_create(&ev);
+    LKV_CUDA(cudaEventRecord(ev, st));
+    tier.used(slots.data(), static_cast<long long>(slots.size()), ev, write);  // takes the event
+  }
   int* d_table = nullptr;      // [max_requests][L][max_blocks]
   int* d_snap = nullptr;       // [L][arena_slots]
   SeqDesc* d_seqs = nullptr;   // [max_batch]
@@ -241,9 +263,14 @@ struct lkv_device final : layersim::KvObserver {
     if (frames > 0x7FFFFFFFll) throw CapacityError("pool + arena frames exceed int32 indexing");
     LKV_CUDA(cudaMalloc(&dbuf, std::max<long long>(frames, 1) * sb));
 
-    if (cfg.host_slots > 0)
+    if (cfg.pinned_frames > 0 && cfg.host_slots > 0) {  // tiered: homes pageable, frames pinned
+      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb);
+      host_pool = tier.pinned();
+      LKV_CUDA(cudaMalloc(&d_xlat, cfg.host_slots * sizeof(int)));
+    } else if (cfg.host_slots > 0) {
       LKV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool), cfg.host_slots * sb,
                              cudaHostAllocMapped | cudaHostAllocPortable));
+    }
     const long long tbl = static_cast<long long>(cfg.max_requests) * L * cfg.max_blocks;
     LKV_CUDA(cudaMalloc(&d_table, tbl * sizeof(int)));
     LKV_CUDA(cudaMalloc(&d_snap, std::max<long long>(1, static_cast<long long>(L) * cfg.arena_slots) *
@@ -350,7 +377,9 @@ struct lkv_device final : layersim::KvObserver {
     for (auto& kvp : prefill_ev) cudaEventDestroy(kvp.second);
     ring.destroy();
     cudaFree(dbuf);
-    if (host_pool) cudaFreeHost(host_pool);
+    if (host_pool && !tiered()) cudaFreeHost(host_pool);
+    tier.destroy();
+    cudaFree(d_xlat);
     cudaFree(d_table);
     cudaFree(d_snap);
     cudaFree(d_seqs);
@@ -437,7 +466,14 @@ struct lkv_device final : layersim::KvObserver {
 
   void on_manager_destroyed() override { kv = nullptr; }
 
-  void on_release(std::int64_t id, const RequestKv&) override {
+  void on_release(std::int64_t id, const RequestKv& r) override {
+    if (tiered()) {  // the request's CPU slots return to the pool: drop their frames, no write-back
+      std::vector<long long> dead;
+      for (const auto& blk : r.blocks)
+        for (const auto& e : blk.layers)
+          if (e.loc == Loc::Cpu) dead.push_back(e.slot);
+      tier.forget(dead.data(), static_cast<long long>(dead.size()));
+    }
     auto it = row_of.find(id);
     if (it == row_of.end()) return;
     free_rows.push_back(it->second);
@@ -529,15 +565,17 @@ struct lkv_device final : layersim::KvObserver {
     return ms;
   }
 
-  void d2h_segment(int seg, const long long* cpu_frames, long long n) {
+  void d2h_segment(int seg, const long long* cpu_slots, long long n) {
     LKV_CUDA(cudaEventRecord(seg_ready[seg], cs));
     LKV_CUDA(cudaStreamWaitEvent(d2h, seg_ready[seg], 0));
-    std::vector<long long> src(n);
+    std::vector<long long> src(n), slots(cpu_slots, cpu_slots + n), frames;
     for (long long i = 0; i < n; ++i) src[i] = seg * seg_slots + i;
+    host_frames(slots, false, &frames);  // whole frames are overwritten: no read-in
     if (timing) timed_begin(d2h, d2h_timed);
     ostats.d2h_copies +=
-        emit_copies(host_pool, cpu_frames, d_staging, src.data(), n, cudaMemcpyDeviceToHost, d2h);
+        emit_copies(host_pool, frames.data(), d_staging, src.data(), n, cudaMemcpyDeviceToHost, d2h);
     if (timing) timed_end(d2h, d2h_timed);
+    host_done(slots, d2h, true);
     ostats.d2h_bytes_physical += n * sb;
     LKV_CUDA(cudaEventRecord(seg_free[seg], d2h));
   }
@@ -548,7 +586,7 @@ struct lkv_device final : layersim::KvObserver {
     long long tokens = 0;
     for (const auto& e : entries) {
       if (static_cast<long long>(e.cpu_slot) >= cfg.host_slots)
-        throw CapacityError("CPU slot " + std::to_string(e.cpu_slot) + " >= pinned host frames");
+        throw CapacityError("CPU slot " + std::to_string(e.cpu_slot) + " >= host frames");
       tokens += e.filled_tokens;
     }
     for (long long i0 = 0; i0 < n; i0 += seg_slots) {
@@ -585,7 +623,14 @@ struct lkv_device final : layersim::KvObserver {
       cudaEventDestroy(it->second);
       job_ev.erase(it);
     }
-    if (orphaned) return;
+    if (orphaned) {  // the reserved CPU destinations return to the pool: their bytes are dead
+      if (tiered()) {
+        std::vector<long long> dead;
+        for (const auto& e : kv->offload_entries(job_id)) dead.push_back(e.cpu_slot);
+        tier.forget(dead.data(), static_cast<long long>(dead.size()));
+      }
+      return;
+    }
     const int row = row_for(rid);
     for (const auto& e : kv->offload_entries(job_id))
       journal.push_back({tindex(row, e.layer, e.block), ~static_cast<int>(e.cpu_slot), 0});
@@ -683,29 +728,36 @@ struct lkv_device final : layersim::KvObserver {
       h2d_started = true;
     }
     const long long arena0 = cfg.gpu_slots + static_cast<long long>(st) * cfg.arena_slots;
-    std::vector<long long> src, dst;
     const long long copies0 = dstats.h2d_copies;
     if (timing) LKV_CUDA(cudaEventRecord(t_f0[l], h2d));
-    for (const Member& m : members) {
+    std::vector<long long> all_slots, all_frames;
+    std::vector<std::size_t> first(members.size() + 1, 0);
+    std::vector<long long> all_dst;
+    for (std::size_t mi = 0; mi < members.size(); ++mi) {
+      const Member& m = members[mi];
       const RequestKv& r = kv->request(m.id);
-      src.clear();
-      dst.clear();
       long long tok = 0;
       for (int b = 0; b < m.nblk; ++b) {
         if (static_cast<long long>(b) * bs >= m.fetch_len) break;  // the appended token's fresh block
         const auto& e = r.blocks[b].layers[l];
         if (e.loc != Loc::Cpu) continue;
         check_slot(e);
-        src.push_back(e.slot);
-        dst.push_back(arena0 + m.blk_off + b);
+        all_slots.push_back(e.slot);
+        all_dst.push_back(arena0 + m.blk_off + b);
         tok += std::clamp<long long>(m.fetch_len - static_cast<long long>(b) * bs, 0, bs);
       }
-      if (src.empty()) continue;
-      dstats.h2d_copies += emit_copies(dbuf, dst.data(), host_pool, src.data(),
-                                       static_cast<long long>(src.size()), cudaMemcpyHostToDevice, h2d);
-      dstats.h2d_bytes_physical += static_cast<long long>(src.size()) * sb;
+      first[mi + 1] = all_slots.size();
       dstats.h2d_bytes_algorithmic += tok * (sb / bs);
     }
+    host_frames(all_slots, true, &all_frames);  // tiered: read in missing slots from their homes
+    for (std::size_t mi = 0; mi < members.size(); ++mi) {
+      const std::size_t a = first[mi], n = first[mi + 1] - a;
+      if (n == 0) continue;
+      dstats.h2d_copies += emit_copies(dbuf, all_dst.data() + a, host_pool, all_frames.data() + a,
+                                       static_cast<long long>(n), cudaMemcpyHostToDevice, h2d);
+      dstats.h2d_bytes_physical += static_cast<long long>(n) * sb;
+    }
+    host_done(all_slots, h2d, false);
     LKV_CUDA(cudaEventRecord(fetch_done[st], h2d));
     if (timing) {
       LKV_CUDA(cudaEventRecord(t_f1[l], h2d));
@@ -919,6 +971,16 @@ struct lkv_device final : layersim::KvObserver {
     const int n = static_cast<int>(members.size());
     auto* dd = reinterpret_cast<AppendDesc*>(ring.reserve(std::max(n, 1) * sizeof(AppendDesc)));
     bool inflight = false;
+    // host frames the token rows go to (tiered: pinned, read in first)
+    std::vector<long long> hslots, hframes;
+    for (int i = 0; i < n; ++i) {
+      const RequestKv& r = kv->request(members[i].id);
+      const auto& e = r.blocks[members[i].fetch_len / bs].layers[l];
+      if (e.loc == Loc::Gpu && e.offload_in_flight) hslots.push_back(e.dest_slot);
+      if (e.loc == Loc::Cpu) hslots.push_back(e.slot);
+    }
+    host_frames(hslots, true, &hframes);
+    std::size_t hk = 0;
     for (int i = 0; i < n; ++i) {
       const Member& m = members[i];
       const RequestKv& r = kv->request(m.id);
@@ -931,12 +993,12 @@ struct lkv_device final : layersim::KvObserver {
         a.dst[0] = dbuf + static_cast<long long>(e.slot) * sb;
         if (e.offload_in_flight) {
           if (static_cast<long long>(e.dest_slot) >= cfg.host_slots) throw CapacityError("append: dest frame");
-          a.dst[1] = host_pool + static_cast<long long>(e.dest_slot) * sb;
+          a.dst[1] = host_pool + hframes[hk++] * sb;
           inflight = true;
         }
       } else if (e.loc == Loc::Cpu) {
         check_slot(e);
-        a.dst[0] = host_pool + static_cast<long long>(e.slot) * sb;
+        a.dst[0] = host_pool + hframes[hk++] * sb;
         a.dst[1] = dbuf + (arena0 + m.blk_off + b) * sb;
       } else {
         throw layersim::SimulationError("decode append: token slot has no location");
@@ -959,6 +1021,7 @@ struct lkv_device final : layersim::KvObserver {
       dstats.kernel_launches += 1;
     }
     ring.commit(cs);
+    host_done(hslots, cs, true);
     appended[l] = 1;
     join_out(user);
   }
@@ -1466,17 +1529,38 @@ static void request_pass(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t s
   if (!write) LKV_CUDA(cudaMemsetAsync(d->d_counter, 0, sizeof(unsigned long long), d->cs));
   // Host frames may still be landing from D2H copies.
   LKV_CUDA(cudaStreamSynchronize(d->d2h));
-  if (nb > 0) {
-    dim3 grid(static_cast<unsigned>(nb), d->L);
+  // Tiered: one layer at a time, its CPU slots pinned (read in) and their
+  // frames published to the kernel through d_xlat.
+  const int passes = d->tiered() ? d->L : 1;
+  for (int p = 0; p < passes && nb > 0; ++p) {
+    std::vector<long long> slots, frames;
+    if (d->tiered()) {
+      for (long long b = 0; b < nb; ++b) {
+        const auto& e = r.blocks[b].layers[p];
+        if (e.loc == Loc::Cpu) slots.push_back(e.slot);
+      }
+      d->host_frames(slots, true, &frames);
+      if (!slots.empty()) {
+        auto* up = reinterpret_cast<TableUpdate*>(d->ring.reserve(slots.size() * sizeof(TableUpdate)));
+        for (std::size_t i = 0; i < slots.size(); ++i) up[i] = {slots[i], static_cast<int>(frames[i]), 0};
+        table_apply_kernel<<<1, 256, 0, d->cs>>>(up, static_cast<int>(slots.size()), d->d_xlat);
+        LKV_CUDA(cudaGetLastError());
+        d->ring.commit(d->cs);
+      }
+    }
+    const int layer0 = d->tiered() ? p : 0;
+    dim3 grid(static_cast<unsigned>(nb), d->tiered() ? 1 : d->L);
+    const int* xl = d->tiered() ? d->d_xlat : nullptr;
     if (write)
       request_kv_kernel<true><<<grid, 256, 0, d->cs>>>(d->d_table + d->tindex(row, 0, 0), d->cfg.max_blocks,
-                                                       d->L, n_tokens, d->dbuf, d->host_pool, d->sb, d->Hl,
+                                                       layer0, n_tokens, d->dbuf, d->host_pool, xl, d->sb, d->Hl,
                                                        d->head0, d->bs, d->D, seed, d->d_counter);
     else
       request_kv_kernel<false><<<grid, 256, 0, d->cs>>>(d->d_table + d->tindex(row, 0, 0), d->cfg.max_blocks,
-                                                        d->L, n_tokens, d->dbuf, d->host_pool, d->sb, d->Hl,
+                                                        layer0, n_tokens, d->dbuf, d->host_pool, xl, d->sb, d->Hl,
                                                         d->head0, d->bs, d->D, seed, d->d_counter);
     LKV_CUDA(cudaGetLastError());
+    d->host_done(slots, d->cs, write);
   }
   if (!write) {
     unsigned long long h = 0;
@@ -1486,6 +1570,33 @@ static void request_pass(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t s
   } else {
     LKV_CUDA(cudaStreamSynchronize(d->cs));
   }
+}
+
+int lkv_device_read_host_slot(lkv_device* d, int64_t slot, void* dst) {
+  LKV_REQUIRE(d && dst && slot >= 0 && slot < d->cfg.host_slots);
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  LKV_CUDA(cudaStreamSynchronize(d->d2h));
+  LKV_CUDA(cudaStreamSynchronize(d->cs));
+  if (d->tiered())
+    d->tier.read_slot(slot, dst);
+  else
+    std::memcpy(dst, d->host_pool + slot * d->sb, static_cast<std::size_t>(d->sb));
+  LKV_CATCH
+}
+
+int lkv_device_host_tier_stats(const lkv_device* d, lkv_host_tier_stats* o) {
+  LKV_REQUIRE(d && o);
+  std::memset(o, 0, sizeof *o);
+  if (d->tier.enabled()) {
+    const auto t = d->tier.stats();
+    o->pinned_frames = d->tier.frames();
+    o->read_in_frames = t.read_in_frames;
+    o->write_back_frames = t.write_back_frames;
+    o->evictions = t.evictions;
+    o->hits = t.hits;
+    o->misses = t.misses;
+  }
+  return LKV_OK;
 }
 
 int lkv_verify_request(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t seed,

@@ -457,15 +457,16 @@ __global__ void fill_kv_tokens_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat
 // mirror: GPU slot -> device pool, ~cpu_slot -> pinned host pool (read or
 // written directly over the link).
 template <bool kWrite>
-__global__ void request_kv_kernel(const int* __restrict__ table_row, int max_blocks, int n_layers,
+__global__ void request_kv_kernel(const int* __restrict__ table_row, int max_blocks, int layer0,
                                   long long n_tokens, char* __restrict__ pool,
-                                  char* __restrict__ host_pool, long long slot_bytes, int Hl,
-                                  int head0, int bs, int D, unsigned long long seed,
-                                  unsigned long long* __restrict__ mismatches) {
-  const int b = blockIdx.x, l = blockIdx.y;
+                                  char* __restrict__ host_pool, const int* __restrict__ xlat,
+                                  long long slot_bytes, int Hl, int head0, int bs, int D,
+                                  unsigned long long seed, unsigned long long* __restrict__ mismatches) {
+  const int b = blockIdx.x, l = layer0 + static_cast<int>(blockIdx.y);
   const int e = table_row[static_cast<long long>(l) * max_blocks + b];
-  char* slot = e >= 0 ? pool + static_cast<long long>(e) * slot_bytes
-                      : host_pool + static_cast<long long>(~e) * slot_bytes;
+  // CPU slot ~e: its pinned frame (tiered host memory: through xlat)
+  const long long hf = e >= 0 ? 0 : (xlat ? xlat[~e] : ~e);
+  char* slot = e >= 0 ? pool + static_cast<long long>(e) * slot_bytes : host_pool + hf * slot_bytes;
   // 16 B per access: host frames are read/written over the link, where
   // narrow accesses would be transaction-bound.
   uint4* s128 = reinterpret_cast<uint4*>(slot);

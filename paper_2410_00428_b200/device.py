@@ -29,11 +29,12 @@ class DeviceConfig:
     max_batch: int = 64
     staging_chunks: int = 4
     chunk_bytes: int = 16 << 20
+    pinned_frames: int = 0  # > 0: tiered host memory (pageable homes + this many pinned frames)
 
     def c(self):
         return _abi.DeviceConfig(self.device, self.tp_rank, self.tp_size, self.pipeline_depth, self.gpu_slots,
                                  self.host_slots, self.arena_slots, self.max_requests, self.max_blocks,
-                                 self.max_batch, self.staging_chunks, self.chunk_bytes)
+                                 self.max_batch, self.staging_chunks, self.chunk_bytes, self.pinned_frames)
 
 
 def _ptr(t) -> int:
@@ -221,8 +222,13 @@ class Device:
 
     # ------------------------------------------------------------- raw views (tests)
     def read_host_slot(self, slot: int) -> bytes:
-        """Bytes of one pinned host frame (CPU slot) — the host pool is
-        ordinary pinned memory, readable directly."""
-        self.synchronize()
-        n = self.slot_bytes
-        return C.string_at(self.info.host_pool + slot * n, n)
+        """Bytes of one CPU slot, wherever they live (pinned frame, or its
+        pageable home in tiered mode)."""
+        buf = C.create_string_buffer(self.slot_bytes)
+        self._lib.call("lkv_device_read_host_slot", self.handle, slot, buf)
+        return buf.raw
+
+    def host_tier_stats(self) -> _abi.HostTierStats:
+        s = _abi.HostTierStats()
+        self._lib.call("lkv_device_host_tier_stats", self.handle, C.byref(s))
+        return s

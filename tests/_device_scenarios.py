@@ -24,12 +24,15 @@ def gqa_model(L=4, hkv=8, group=4, d=128):
 
 
 def make(model, bs=16, gpu=512, cpu=512, tp_rank=0, tp_size=1, depth=2, chunk_slots=3, max_blocks=64,
-         max_batch=8, arena=None):
+         max_batch=8, arena=None, pinned=0):
+    """pinned > 0: tiered host memory (pageable homes for all `cpu` slots,
+    `pinned` pinned frames)."""
     kv = ls.KvManager(ls.BlockPools(gpu, cpu, bs), model)
     slot_bytes = 2 * (model.n_kv_heads // tp_size) * bs * model.d_head * 2
     cfg = DeviceConfig(device=0, tp_rank=tp_rank, tp_size=tp_size, pipeline_depth=depth, gpu_slots=gpu,
                        host_slots=cpu, arena_slots=arena or gpu, max_requests=16, max_blocks=max_blocks,
-                       max_batch=max_batch, staging_chunks=4, chunk_bytes=chunk_slots * slot_bytes)
+                       max_batch=max_batch, staging_chunks=4, chunk_bytes=chunk_slots * slot_bytes,
+                       pinned_frames=pinned)
     dev = Device(kv, model, bs, cfg)
     return kv, dev
 
