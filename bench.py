@@ -441,6 +441,60 @@ def gqa_decode_row(torch, dev_t, hbm_peak, hq=32, hkv=8, tp_size=1, B=16, ctx=32
             "frac_with_merge": byts / ((best + merge) / 1e3) / 1e9 / hbm_peak}
 
 
+def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=3):
+    """f3: config 2's decode iteration (7B, every layer CPU-resident) with the
+    CPU slots' homes in pageable memory and only `pinned_frac` of them backed
+    by pinned frames. The layer-ordered re-fetch cycles through more slots
+    than there are frames, so nearly every prefetch reads its slot back in
+    from the pageable home (parallel memcpy) before the DMA: this row measures
+    what the pageable tier costs against the all-pinned headline."""
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+    model = ls.llama2_7b()
+    L, bs = model.n_layers, 16
+    nblk = ctx // bs
+    slots = B * nblk * L
+    pinned = int(slots * pinned_frac)
+    kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model)
+    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=64, host_slots=slots + 64,
+                                             arena_slots=B * nblk + 16, max_requests=B + 1, max_blocks=nblk + 4,
+                                             max_batch=B, pinned_frames=pinned))
+    ids = list(range(B))
+    for r in ids:
+        assert kv.allocate_prefill(r, ctx, 0)
+        dev.fill_request(r, ctx, SEED)
+    q = torch.randn((B, dev.q_heads_local, 128), dtype=torch.bfloat16, device=dev_t)
+    out = torch.empty_like(q)
+    cs = dev.torch_stream("compute")
+    dev.set_timing(True)
+    t0s = dev.host_tier_stats()
+    times = []
+    for it in range(steps + 1):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        dev.decode_begin(ids)
+        for layer in range(L):
+            dev.decode_layer(layer, q, out, 1 / math.sqrt(128), DTYPE_BF16, stream=cs)
+        dev.decode_end()
+        dev.synchronize()
+        if it >= 1:
+            times.append(time.perf_counter() - t0)
+    st = dev.decode_stats()
+    t1s = dev.host_tier_stats()
+    bad = dev.verify_request(B - 1, ctx, SEED)
+    dev.close()
+    step_s = min(times)
+    fetch = st.h2d_bytes_algorithmic
+    return {"workload": f"{B} x {ctx} tokens, 7B, all {L} layers CPU-resident; {pinned} pinned frames for {slots} "
+                        f"CPU slots ({pinned_frac:.0%}), homes pageable",
+            "step_s": step_s, "prefetch_gbs": fetch / step_s / 1e9, "link_h2d_peak_gbs": link["h2d"],
+            "frac_of_link": fetch / step_s / 1e9 / link["h2d"],
+            "read_in_frames_per_step": (t1s.read_in_frames - t0s.read_in_frames) / (steps + 1),
+            "hit_rate": (t1s.hits - t0s.hits) / max(1, (t1s.hits - t0s.hits) + (t1s.misses - t0s.misses)),
+            "kv_verified_mismatches": bad,
+            "timing": "wall clock around decode_begin..synchronize (host read-ins are on the critical path)"}
+
+
 def serving_row(link, tf_peak, hbm_peak, n=6, prompt=16384, output=8, rate=8.0):
     """f1: the product's serving loop on config 2's shape (7B, 48 GB-capped
     pools, LayerKV policy, fixed 16k prompts arriving fast enough to force
@@ -686,6 +740,7 @@ def main():
             rows["a18_gqa_decode_70b_tp8_shard"] = gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8, tp_size=8,
                                                                   B=64, ctx=32768, label="70B GQA TP8 rank 0")
             rows["f1_measured_serving"] = serving_row(link, tensor_peak(), hbm_peak)
+            rows["f3_tiered_host_decode"] = tiered_host_row(torch, dev_t, link)
             line["rows"] = rows
         print(json.dumps(line), flush=True)
     if world > 1:

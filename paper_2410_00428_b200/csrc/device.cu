@@ -264,7 +264,8 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaMalloc(&dbuf, std::max<long long>(frames, 1) * sb));
 
     if (cfg.pinned_frames > 0 && cfg.host_slots > 0) {  // tiered: homes pageable, frames pinned
-      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb);
+      const int cores = static_cast<int>(std::thread::hardware_concurrency());
+      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb, std::clamp(cores, 2, 16));
       host_pool = tier.pinned();
       LKV_CUDA(cudaMalloc(&d_xlat, cfg.host_slots * sizeof(int)));
     } else if (cfg.host_slots > 0) {
@@ -518,14 +519,41 @@ struct lkv_device final : layersim::KvObserver {
       const long long len = j - i;
       char* d = dst_base + dst_frames[i] * sb;
       const char* sp = src_base + src_frames[i] * sb;
-      if (len == 1 || (dd == 1 && ds == 1)) {
-        LKV_CUDA(cudaMemcpyAsync(d, sp, len * sb, kind, s));
+      if (len == 1 || (dd == 1 && ds == 1)) {  // contiguous: one linear copy (batched below)
+        b_dst.push_back(d);
+        b_src.push_back(const_cast<char*>(sp));
+        b_size.push_back(static_cast<std::size_t>(len * sb));
       } else {
         LKV_CUDA(cudaMemcpy2DAsync(d, dd * sb, sp, ds * sb, sb, len, kind, s));
+        ++copies;
       }
-      ++copies;
       i = j;
     }
+    copies += flush_linear(kind, s);
+    return copies;
+  }
+
+  // Linear copies of one emit_copies call: a single cudaMemcpyBatchAsync when
+  // there are several (scattered frames, e.g. tiered host frames), instead of
+  // one API call per frame.
+  std::vector<void*> b_dst, b_src;
+  std::vector<std::size_t> b_size;
+  int flush_linear(cudaMemcpyKind kind, cudaStream_t s) {
+    const std::size_t n = b_dst.size();
+    int copies = 0;
+    if (n == 1 || (n > 1 && s == nullptr)) {
+      for (std::size_t k = 0; k < n; ++k) LKV_CUDA(cudaMemcpyAsync(b_dst[k], b_src[k], b_size[k], kind, s));
+      copies = static_cast<int>(n);
+    } else if (n > 1) {
+      cudaMemcpyAttributes attr{};
+      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+      std::size_t idx0 = 0, fail = 0;
+      LKV_CUDA(cudaMemcpyBatchAsync(b_dst.data(), b_src.data(), b_size.data(), n, &attr, &idx0, 1, &fail, s));
+      copies = 1;
+    }
+    b_dst.clear();
+    b_src.clear();
+    b_size.clear();
     return copies;
   }
 

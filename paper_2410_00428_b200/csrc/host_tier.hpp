@@ -63,7 +63,9 @@ class HostTier {
     slot_frame_.assign(static_cast<std::size_t>(S_), -1);
     slot_valid_.assign(static_cast<std::size_t>(S_), 0);
     frames_.resize(static_cast<std::size_t>(F_));
-    for (long long f = 0; f < F_; ++f) free_.push_back(static_cast<int>(f));
+    // popped from the back: ascending frames, so a batch of misses gets a
+    // contiguous run and its DMA coalesces into one copy
+    for (long long f = F_ - 1; f >= 0; --f) free_.push_back(static_cast<int>(f));
     threads_ = std::max(1, copy_threads);
     stop_ = false;
     cleaner_ = std::thread([this] { clean_loop(); });
