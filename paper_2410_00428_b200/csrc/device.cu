@@ -26,6 +26,7 @@
 #include "decode_attn.cuh"
 #include "decode_gqa_tc.cuh"
 #include "prefill_attn.cuh"
+#include "prefill_attn2.cuh"
 #include "host_tier.hpp"
 #include "kernels.cuh"
 #include "layersim/errors.hpp"
@@ -1295,10 +1296,8 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   const uint64_t T = static_cast<uint64_t>(tokens), D = static_cast<uint64_t>(d->D);
   // LKV_PREFILL_P=bf16x2: P as bf16 hi + lo against bf16 V (two PV MMAs);
   // default fp16 P against an fp16 copy of V (one PV MMA).
-  static const bool pf16 = [] {
-    const char* e = std::getenv("LKV_PREFILL_P");
-    return !(e && std::strcmp(e, "bf16x2") == 0);
-  }();
+  const char* ep = std::getenv("LKV_PREFILL_P");
+  const bool pf16 = !(ep && std::strcmp(ep, "bf16x2") == 0);
   const void* vsrc = v;
   if (pf16) {  // fp16 copy of V in a device scratch (bf16 -> fp16 is exact in fp16's normal range)
     const std::size_t need = static_cast<std::size_t>(T) * d->Hl * D * 2;
@@ -1326,6 +1325,22 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
     const char* e = std::getenv("LKV_PREFILL_WG");
     return (e && std::atoi(e) == 1) ? 1 : 2;
   }();
+  // LKV_PREFILL_KERNEL=1: the one-tile kernel (row halves); default with fp16
+  // P: two query tiles per CTA, one softmax warpgroup each (prefill_attn2.cuh).
+  const char* ek = std::getenv("LKV_PREFILL_KERNEL");
+  const bool two_tile = !(ek && std::atoi(ek) == 1);
+  if (pf16 && two_tile) {
+    d->smem_attr(reinterpret_cast<const void*>(prefill_attn2_kernel), PrefillAttn2Smem::kBytes);
+    const int nq = static_cast<int>((tokens + 127) / 128);
+    const dim3 grid2(static_cast<unsigned>((nq + 1) / 2), static_cast<unsigned>(d->Hql));
+    prefill_attn2_kernel<<<grid2, 320, PrefillAttn2Smem::kBytes, s>>>(
+        qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
+        scale * 1.4426950408889634f);
+    LKV_CUDA(cudaGetLastError());
+    LKV_CUDA(cudaEventRecord(d->vh_free, s));
+    d->vh_used = true;
+    return LKV_OK;
+  }
   auto fn = nwg == 1 ? (pf16 ? prefill_attn_kernel<1, true> : prefill_attn_kernel<1, false>)
                      : (pf16 ? prefill_attn_kernel<2, true> : prefill_attn_kernel<2, false>);
   d->smem_attr(reinterpret_cast<const void*>(fn), PrefillAttnSmem::kBytes);

@@ -1,0 +1,277 @@
+// Causal GQA prefill attention, two query tiles per CTA.
+//
+// prefill_attn_kernel splits each S row between two softmax warpgroups; both
+// pass the load -> max -> exp -> store phases of one tile in lockstep, so the
+// MUFU (ex2) idles outside the exp phase and the tensor pipe waits on it
+// (ncu: both ~50% busy). Here a CTA owns query tiles A = 2p and B = 2p + 1
+// of one head and gives each its own softmax warpgroup (thread = query row,
+// all 128 columns), so one tile's exponentials overlap the other's TMEM
+// traffic and the MMAs of the other tile, and every K/V tile loaded from HBM
+// serves 256 query rows.
+//
+// Warps: 0 TMA (Q_A, Q_B, then the K and V rings, 2 stages each; a K stage
+// frees when both S MMAs read it, a V stage when both PVs did), 1 MMA issuer
+// + TMEM owner, 2-5 softmax of tile A, 6-9 softmax of tile B (warp w reads
+// TMEM lanes 32*(w%4)..+31).
+// TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,384),
+// O_B [384,512). P (fp16 pairs, against the fp16 copy of V) overwrites the
+// first 64 columns of its S. Issue order per KV tile j:
+//   ... PV_A(j-1), S_A(j), PV_B(j-1), S_B(j), PV_A(j), ...
+// The tensor pipe executes in issue order, so S_A(j) never overwrites P_A(j-1)
+// before PV_A(j-1) read it. Tile A's causal range is KV tiles 0..2p, B's is
+// 0..2p+1 (the last KV tile is B's alone).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "prefill_attn.cuh"
+#include "tc_sm100.cuh"
+
+namespace lkv {
+
+struct PrefillAttn2Smem {
+  static constexpr int kStages = 2;
+  static constexpr int kQ = 0;                       // Q_A, Q_B: 2 x 32 KiB
+  static constexpr int kK = 65536;                   // kStages x 32 KiB
+  static constexpr int kV = kK + kStages * 32768;    // kStages x 32 KiB
+  static constexpr int kBar = kV + kStages * 32768;  // mbarriers
+  static constexpr int kNumBars = 1 + 2 * 3 + 4 * kStages;
+  static constexpr int kTmem = kBar + kNumBars * 8;
+  static constexpr int kBytes = kTmem + 16;
+  static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
+};
+
+__global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
+    const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
+    const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
+    float scale_log2) {
+  using S = PrefillAttn2Smem;
+  constexpr int NS = S::kStages;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* sm = smem_raw;
+  if ((tc::saddr(sm) & 1023u) != 0u) __trap();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::kBar);
+  uint64_t* q_full = bars;
+  uint64_t* s_full = bars + 1;  // [2] tile A, B
+  uint64_t* p_full = bars + 3;  // [2]
+  uint64_t* o_full = bars + 5;  // [2]
+  uint64_t* k_full = bars + 7;  // [NS]
+  uint64_t* k_empty = k_full + NS;
+  uint64_t* v_full = k_empty + NS;
+  uint64_t* v_empty = v_full + NS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(sm + S::kTmem);
+
+  const int nq = (tokens + 127) / 128;
+  const int npairs = (nq + 1) / 2;
+  const int pair = npairs - 1 - static_cast<int>(blockIdx.x);  // heaviest first
+  const int qa = 2 * pair, qb = 2 * pair + 1;
+  const bool has_b = qb < nq;
+  const int nt_a = qa + 1, nt_b = has_b ? qb + 1 : 0;
+  const int nt = has_b ? nt_b : nt_a;  // KV tiles this CTA loads
+  const int hq = blockIdx.y, h = hq / G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    tc::bar_init(q_full, 1);
+    for (int t = 0; t < 2; ++t) {
+      tc::bar_init(&s_full[t], 1);
+      tc::bar_init(&p_full[t], 128);
+      tc::bar_init(&o_full[t], 1);
+    }
+    for (int b = 0; b < NS; ++b) {
+      tc::bar_init(&k_full[b], 1);
+      tc::bar_init(&k_empty[b], 1);
+      tc::bar_init(&v_full[b], 1);
+      tc::bar_init(&v_empty[b], 1);
+    }
+    tc::bar_fence_init();
+  }
+  if (warp == 1) tc::tmem_alloc<512>(tmem_slot);
+  tc::fence_before_sync();
+  __syncthreads();
+  tc::fence_after_sync();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      tc::tma_prefetch_desc(&qmap);
+      tc::tma_prefetch_desc(&kmap);
+      tc::tma_prefetch_desc(&vmap);
+      tc::bar_expect_tx(q_full, has_b ? 65536 : 32768);
+      tc::tma_load_3d(sm + S::kQ, &qmap, 0, hq, qa * 128, q_full);
+      tc::tma_load_3d(sm + S::kQ + 16384, &qmap, 64, hq, qa * 128, q_full);
+      if (has_b) {
+        tc::tma_load_3d(sm + S::kQ + 32768, &qmap, 0, hq, qb * 128, q_full);
+        tc::tma_load_3d(sm + S::kQ + 49152, &qmap, 64, hq, qb * 128, q_full);
+      }
+      // K(j) then V(j): K runs a tile ahead of V in the MMA order below
+      for (int j = 0; j < nt; ++j) {
+        const int st = j % NS;
+        const uint32_t ph = ((j / NS) & 1u) ^ 1u;
+        tc::bar_wait(&k_empty[st], ph);
+        tc::bar_expect_tx(&k_full[st], 32768);
+        uint8_t* kt = sm + S::kK + st * 32768;
+        tc::tma_load_3d(kt, &kmap, 0, h, j * 128, &k_full[st]);
+        tc::tma_load_3d(kt + 16384, &kmap, 64, h, j * 128, &k_full[st]);
+        tc::bar_wait(&v_empty[st], ph);
+        tc::bar_expect_tx(&v_full[st], 32768);
+        uint8_t* vt = sm + S::kV + st * 32768;
+        tc::tma_load_3d(vt, &vmap, 0, h, j * 128, &v_full[st]);
+        tc::tma_load_3d(vt + 16384, &vmap, 64, h, j * 128, &v_full[st]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idS = tc::idesc_bf16(128, 128, false, false);
+      constexpr uint32_t idO = tc::idesc_f16(128, 128, false, true);
+      const uint32_t q0 = tc::saddr(sm + S::kQ), k0 = tc::saddr(sm + S::kK), v0 = tc::saddr(sm + S::kV);
+      auto qk = [&](int t, int j) {  // S_t(j) = Q_t K_j^T
+        const uint32_t qt = q0 + t * 32768, kt = k0 + (j % NS) * 32768;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t o = (kk >> 2) * 16384 + (kk & 3) * 32;
+          tc::mma_bf16(tmem + t * 128, tc::smem_desc(qt + o, 16, 1024, tc::kLayoutSw128),
+                       tc::smem_desc(kt + o, 16, 1024, tc::kLayoutSw128), idS, kk > 0);
+        }
+        tc::mma_commit(&s_full[t]);
+      };
+      auto pv = [&](int t, int j) {  // O_t += P_t(j) V_j
+        tc::bar_wait(&p_full[t], j & 1u);
+        tc::fence_after_sync();
+        const uint32_t vt = v0 + (j % NS) * 32768;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint64_t bd = tc::smem_desc(vt + kk * 2048, 16384, 1024, tc::kLayoutSw128);
+          tc::mma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, bd, idO, (j > 0 || kk > 0));
+        }
+        tc::mma_commit(&o_full[t]);
+      };
+      tc::bar_wait(q_full, 0);
+      for (int j = 0; j <= nt; ++j) {
+        // PV of KV tile j-1 for each tile that covers it, each followed by
+        // that tile's S of KV tile j (issue order = execution order)
+        if (j > 0) {
+          const int jp = j - 1;
+          tc::bar_wait(&v_full[jp % NS], (jp / NS) & 1u);
+          tc::fence_after_sync();
+        }
+        if (j < nt) {
+          tc::bar_wait(&k_full[j % NS], (j / NS) & 1u);
+          tc::fence_after_sync();
+        }
+        if (j > 0 && j - 1 < nt_a) pv(0, j - 1);
+        if (j < nt_a) qk(0, j);
+        if (j > 0 && j - 1 < nt_b) pv(1, j - 1);
+        if (j < nt_b) qk(1, j);
+        if (j < nt) tc::mma_commit(&k_empty[j % NS]);
+        if (j > 0) tc::mma_commit(&v_empty[(j - 1) % NS]);
+      }
+    }
+  } else {
+    // softmax: warpgroup t (0 = tile A, 1 = tile B), thread = query row
+    const int t = (warp - 2) >> 2;
+    const int quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const int qt = t == 0 ? qa : qb;
+    const int ntt = t == 0 ? nt_a : nt_b;
+    const int row = qt * 128 + r;
+    const uint32_t tl = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+    const uint32_t s_col = t * 128, o_col = 256 + t * 128;
+    float m_run = -INFINITY, l_run = 0.f;
+    float s[128];
+    for (int j = 0; j < ntt; ++j) {
+      tc::bar_wait(&s_full[t], j & 1u);
+      tc::fence_after_sync();
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tl + s_col + c * 32, s + c * 32);
+      tc::tmem_wait_ld();
+      if (j == qt) {  // diagonal tile: key j*128 + c <= row
+#pragma unroll
+        for (int c = 0; c < 128; ++c) s[c] = (c <= r) ? s[c] : -INFINITY;
+      }
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+      for (int c = 0; c < 128; ++c) mx[c & 3] = fmaxf(mx[c & 3], s[c]);
+      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+      float corr = 1.f;
+      bool resc = false;
+      if (mt > m_run + 8.f) {  // lazy rescale (see prefill_attn.cuh)
+        corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
+        resc = j > 0;
+        m_run = mt;
+        l_run *= corr;
+      }
+      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {  // P(j) -> TMEM over S(j), 32 columns at a time
+        uint32_t ph[16];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float a = ex2_approx(fmaf(s[c * 32 + 2 * i], scale_log2, -m_run));
+          const float b = ex2_approx(fmaf(s[c * 32 + 2 * i + 1], scale_log2, -m_run));
+          ls[i & 3] += a + b;
+          const __half2 h2 = __floats2half2_rn(a, b);
+          ph[i] = *reinterpret_cast<const uint32_t*>(&h2);
+        }
+        tc::tmem_st16(tl + s_col + c * 16, ph);
+      }
+      l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      if (__any_sync(0xffffffffu, resc)) {  // O must hold PV(j-1) before it is rescaled
+        tc::bar_wait(&o_full[t], (j - 1) & 1u);
+        tc::fence_after_sync();
+        const float f = resc ? corr : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float o[32];
+          tc::tmem_ld32(tl + o_col + c * 32, o);
+          tc::tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) o[i] *= f;
+          tc::tmem_st32(tl + o_col + c * 32, o);
+        }
+      }
+      tc::tmem_wait_st();
+      tc::fence_before_sync();
+      tc::bar_arrive(&p_full[t]);
+    }
+    if (ntt > 0) {
+      tc::bar_wait(&o_full[t], (ntt - 1) & 1u);
+      tc::fence_after_sync();
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const long long obase = (static_cast<long long>(row) * Hq + hq) * 128;
+      __nv_bfloat16* dst = static_cast<__nv_bfloat16*>(out) + obase;
+      float* dstf = static_cast<float*>(out) + obase;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        float o[32];
+        tc::tmem_ld32(tl + o_col + c * 32, o);
+        tc::tmem_wait_ld();
+        if (row < tokens && out_f32) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            *reinterpret_cast<float4*>(dstf + c * 32 + i * 4) =
+                make_float4(o[4 * i] * inv, o[4 * i + 1] * inv, o[4 * i + 2] * inv, o[4 * i + 3] * inv);
+        } else if (row < tokens) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            uint4 v;
+            v.x = tc::pack_bf16(o[8 * i + 0] * inv, o[8 * i + 1] * inv);
+            v.y = tc::pack_bf16(o[8 * i + 2] * inv, o[8 * i + 3] * inv);
+            v.z = tc::pack_bf16(o[8 * i + 4] * inv, o[8 * i + 5] * inv);
+            v.w = tc::pack_bf16(o[8 * i + 6] * inv, o[8 * i + 7] * inv);
+            *reinterpret_cast<uint4*>(dst + c * 32 + i * 8) = v;
+          }
+        }
+      }
+    }
+  }
+  tc::fence_before_sync();
+  __syncthreads();
+  if (warp == 1) tc::tmem_free<512>(tmem);
+}
+
+}  // namespace lkv
