@@ -1330,10 +1330,14 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   const char* ek = std::getenv("LKV_PREFILL_KERNEL");
   const bool two_tile = !(ek && std::atoi(ek) == 1);
   if (pf16 && two_tile) {
-    d->smem_attr(reinterpret_cast<const void*>(prefill_attn2_kernel), PrefillAttn2Smem::kBytes);
+    // LKV_PREFILL_POLY = 0 / 25 / 50: share of exponentials computed on the FMA pipe
+    const char* epo = std::getenv("LKV_PREFILL_POLY");
+    const int poly = epo ? std::atoi(epo) : 0;
+    auto fn2 = poly >= 50 ? prefill_attn2_kernel<2> : poly >= 25 ? prefill_attn2_kernel<1> : prefill_attn2_kernel<0>;
+    d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
     const int nq = static_cast<int>((tokens + 127) / 128);
     const dim3 grid2(static_cast<unsigned>((nq + 1) / 2), static_cast<unsigned>(d->Hql));
-    prefill_attn2_kernel<<<grid2, 320, PrefillAttn2Smem::kBytes, s>>>(
+    fn2<<<grid2, 320, PrefillAttn2Smem::kBytes, s>>>(
         qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
         scale * 1.4426950408889634f);
     LKV_CUDA(cudaGetLastError());

@@ -45,6 +45,43 @@ struct PrefillAttn2Smem {
   static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
 };
 
+// 2^x on the FMA/ALU pipes (x <= ~126): round-to-nearest split x = n + f
+// with the 1.5*2^23 trick, a degree-3 fit of 2^f on [-0.5, 0.5] (max relative
+// error 1.03e-4, below fp16 P's 2^-11 rounding), n added to the exponent.
+// x = -inf (masked) clamps to 2^-127 -> 0 in fp16. Takes a share of the
+// softmax exponentials off the MUFU, which bounds the softmax warpgroup.
+__device__ __forceinline__ float ex2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float t = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
+  const float p = fmaf(fmaf(fmaf(0.05500683f, f, 0.2422056f), f, 0.69328254f), f, 1.0f);
+  const int n = __float_as_int(t) - 0x4B400000;
+  return __int_as_float(__float_as_int(p) + (n << 23));
+}
+
+// Packed fp32x2 FMA / add (sm_100 FFMA2 / FADD2): half the issue slots of
+// the softmax's scale-subtract and row-sum.
+__device__ __forceinline__ unsigned long long f2pack(float a, float b) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+  return r;
+}
+__device__ __forceinline__ void f2unpack(unsigned long long v, float& a, float& b) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+__device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+
+// POLY: of every 4 column pairs, this many use ex2_poly (0, 1 or 2).
+template <int POLY>
 __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
@@ -205,21 +242,30 @@ __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
         m_run = mt;
         l_run *= corr;
       }
-      float ls[4] = {0.f, 0.f, 0.f, 0.f};
+      unsigned long long ls2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
+      const unsigned long long sc2 = f2pack(scale_log2, scale_log2), nm2 = f2pack(-m_run, -m_run);
 #pragma unroll
       for (int c = 0; c < 4; ++c) {  // P(j) -> TMEM over S(j), 32 columns at a time
         uint32_t ph[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
-          const float a = ex2_approx(fmaf(s[c * 32 + 2 * i], scale_log2, -m_run));
-          const float b = ex2_approx(fmaf(s[c * 32 + 2 * i + 1], scale_log2, -m_run));
-          ls[i & 3] += a + b;
+          float xa, xb;
+          f2unpack(ffma2(f2pack(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2), xa, xb);
+          const bool poly = (i & 3) >= 4 - POLY;
+          const float a = poly ? ex2_poly(xa) : ex2_approx(xa);
+          const float b = poly ? ex2_poly(xb) : ex2_approx(xb);
+          ls2[i & 1] = fadd2(ls2[i & 1], f2pack(a, b));
           const __half2 h2 = __floats2half2_rn(a, b);
           ph[i] = *reinterpret_cast<const uint32_t*>(&h2);
         }
         tc::tmem_st16(tl + s_col + c * 16, ph);
       }
-      l_run += (ls[0] + ls[1]) + (ls[2] + ls[3]);
+      {
+        float l0, l1, l2, l3;
+        f2unpack(ls2[0], l0, l1);
+        f2unpack(ls2[1], l2, l3);
+        l_run += (l0 + l1) + (l2 + l3);
+      }
       if (__any_sync(0xffffffffu, resc)) {  // O must hold PV(j-1) before it is rescaled
         tc::bar_wait(&o_full[t], (j - 1) & 1u);
         tc::fence_after_sync();

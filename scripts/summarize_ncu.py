@@ -19,39 +19,41 @@ tag = sys.argv[1] if len(sys.argv) > 1 else "r1"
 out_dir = os.path.join(ROOT, "profiles")
 os.makedirs(out_dir, exist_ok=True)
 
-# ---- launch list
+# ---- launch list (when this tag has one)
 path = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
-with open(path) as f:
-    lines = [l for l in f if l.startswith('"')]
-rows = list(csv.reader(io.StringIO("".join(lines))))
-hdr = rows[0]
-ki, mi, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-agg = collections.OrderedDict()
-for r in rows[1:]:
-    if r[mi] != "gpu__time_duration.sum":
-        continue
-    name = r[ki].split("(")[0].replace("void ", "")
-    scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
-    t = float(r[vi].replace(",", "")) * scale
-    c = agg.setdefault(name, [0, 0.0])
-    c[0] += 1
-    c[1] += t
-STEP = ("decode_attn_v2", "decode_attn_kernel", "decode_merge", "decode_snapshot")
-ROWS = ("prefill_attn", "decode_gqa_tc")
-with open(os.path.join(out_dir, f"{tag}_launches.txt"), "w") as f:
-    f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none of: python bench.py --steps 2 --warmup 1"
-            f" --no-cpu-baseline\n# per-launch times are serialised/cold-cache: compare shares, not absolutes\n")
-    for title, sel in (("decode-step kernels (the timed region)", lambda k: any(x in k for x in STEP)),
-                       ("tensor-core rows beside the headline (prefill attention, GQA decode tile)",
-                        lambda k: any(x in k for x in ROWS)),
-                       ("setup kernels (prefill offload, synthetic data, verification)",
-                        lambda k: not any(x in k for x in STEP + ROWS))):
-        part = {k: v for k, v in agg.items() if sel(k)}
-        total = sum(v[1] for v in part.values()) or 1.0
-        f.write(f"\n## {title}\n{'kernel':50s} {'launches':>9s} {'total_us':>12s} {'avg_us':>10s} {'share':>7s}\n")
-        for k, (n, t) in sorted(part.items(), key=lambda kv: -kv[1][1]):
-            f.write(f"{k[:50]:50s} {n:9d} {t:12.1f} {t / n:10.2f} {100 * t / total:6.2f}%\n")
-print(open(os.path.join(out_dir, f"{tag}_launches.txt")).read())
+if os.path.exists(path):
+    with open(path) as f:
+        lines = [l for l in f if l.startswith('"')]
+    rows = list(csv.reader(io.StringIO("".join(lines))))
+    hdr = rows[0]
+    ki, mi, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    agg = collections.OrderedDict()
+    for r in rows[1:]:
+        if r[mi] != "gpu__time_duration.sum":
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(r[ui], 1.0)
+        t = float(r[vi].replace(",", "")) * scale
+        c = agg.setdefault(name, [0, 0.0])
+        c[0] += 1
+        c[1] += t
+    STEP = ("decode_attn_v2", "decode_attn_kernel", "decode_merge", "decode_snapshot")
+    ROWS = ("prefill_attn", "decode_gqa_tc")
+    with open(os.path.join(out_dir, f"{tag}_launches.txt"), "w") as f:
+        f.write(f"# ncu --metrics gpu__time_duration.sum --clock-control none of: python bench.py --steps 2 --warmup 1"
+                f" --no-cpu-baseline\n# per-launch times are serialised/cold-cache: compare shares, not absolutes\n")
+        for title, sel in (("decode-step kernels (the timed region)", lambda k: any(x in k for x in STEP)),
+                           ("tensor-core rows beside the headline (prefill attention, GQA decode tile)",
+                            lambda k: any(x in k for x in ROWS)),
+                           ("setup kernels (prefill offload, synthetic data, verification)",
+                            lambda k: not any(x in k for x in STEP + ROWS))):
+            part = {k: v for k, v in agg.items() if sel(k)}
+            total = sum(v[1] for v in part.values()) or 1.0
+            f.write(f"\n## {title}\n{'kernel':50s} {'launches':>9s} {'total_us':>12s} {'avg_us':>10s} {'share':>7s}\n")
+            for k, (n, t) in sorted(part.items(), key=lambda kv: -kv[1][1]):
+                f.write(f"{k[:50]:50s} {n:9d} {t:12.1f} {t / n:10.2f} {100 * t / total:6.2f}%\n")
+    print(open(os.path.join(out_dir, f"{tag}_launches.txt")).read())
+
 
 # ---- full captures of the tensor-core kernels (prefill attention, GQA decode tile)
 TC_KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
@@ -64,8 +66,11 @@ TC_KEYS = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dra
            "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
            "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
            "smsp__warp_issue_stalled_wait_per_warp_active.pct",
-           "smsp__warp_issue_stalled_math_pipe_throttle_per_warp_active.pct"]
-for cap in ("prefill_attn", "decode_gqa_tc"):
+           "smsp__warp_issue_stalled_math_pipe_throttle_per_warp_active.pct",
+           "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+           "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+           "sm__issue_active.avg.pct_of_peak_sustained_elapsed"]
+for cap in ("prefill_attn", "prefill_attn2", "decode_gqa_tc"):
     rep = os.path.join(ROOT, "gpurun_out", f"{cap}_{tag}.ncu-rep")
     if not os.path.exists(rep):
         continue
