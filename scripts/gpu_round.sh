@@ -11,8 +11,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $O/ncu_list_$TAG.log 2>&1; echo "ncu list rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:decode_attn -s 33 -c 2 \
   -o $O/decode_attn_$TAG -f python bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-rows > $O/ncu_full_$TAG.log 2>&1; echo "ncu full rc=$?"
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_attn -c 1 \
-  -o $O/prefill_attn_$TAG -f python scripts/prefill_micro.py --tokens 8192 --iters 1 > $O/ncu_pf_$TAG.log 2>&1; echo "ncu prefill rc=$?"
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_attn2 -c 1 \
+  -o $O/prefill_attn2_$TAG -f python scripts/prefill_micro.py --tokens 8192 --iters 1 > $O/ncu_pf_$TAG.log 2>&1; echo "ncu prefill rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_gqa_tc -c 1 \
   -o $O/decode_gqa_tc_$TAG -f python scripts/attn_micro.py --group 8 --ctx 16384 --batch 8 --layers 1 --iters 1 > $O/ncu_gqa_$TAG.log 2>&1; echo "ncu gqa rc=$?"
 ls -la $O
