@@ -368,9 +368,11 @@ def prefill_rows(torch, dev_t, link, tf_peak):
         dev.synchronize()
         kv.release(0)
         return e0.elapsed_time(e1)
+    dev.set_timing(True)  # copy-engine busy time of the D2H copies (CUDA events around each batch)
     with_ms = min(prefill_with_offload() for _ in range(3))
     ost = dev.offload_stats(reset=True)
     bytes_off = ost.d2h_bytes_algorithmic // 3
+    d2h_busy_ms = ost.d2h_ms / 3
     link_ms = bytes_off / (link["d2h"] * 1e9) * 1e3
     exposed = max(0.0, with_ms - compute_ms)
     # simulated prefill of the same prompt: reference cost model (Eq. 3,
@@ -391,6 +393,7 @@ def prefill_rows(torch, dev_t, link, tf_peak):
             "offload_bytes": bytes_off, "offload_alone_at_link_peak_ms": link_ms,
             "hidden_frac": max(0.0, 1.0 - exposed / link_ms) if link_ms else None,
             "last_layer_offload_at_link_peak_ms": link_ms / L,
+            "d2h_busy_ms": d2h_busy_ms, "d2h_gbs_while_busy": bytes_off / (d2h_busy_ms / 1e3) / 1e9 if d2h_busy_ms else None,
             "timing": "CUDA events: compute stream start -> D2H stream end, min of 3 prefills",
             "offload_gbs_during_prefill": bytes_off / (with_ms / 1e3) / 1e9,
             "layer_tflops": L * (flops + dense_flops) / compute_ms / 1e9,

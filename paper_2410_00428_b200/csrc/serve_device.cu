@@ -96,8 +96,6 @@ class DeviceExecutor final : public lkv::Executor {
       : cfg_(cfg), kv_(kv), o_(o), modelled_(cfg, kv) {
     const auto& m = cfg.model;
     const int bs = cfg.pools.tokens_per_block;
-    const int tp = std::max(1, cfg.hw.n_gpus);
-    (void)tp;
     lkv_model_spec ms{m.n_layers, m.n_heads, m.n_kv_heads, m.d_head, m.hidden, m.n_param, m.f_precision, 0};
     lkv_device_config dc{};
     dc.device = o.device;
