@@ -351,7 +351,6 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     attn_ms = min(ev_ms(torch, cs, attn) for _ in range(3))
     flops = 4.0 * d * hq * T * (T + 1) / 2
     # whole prompt: per-layer compute, then the same with the offload of every layer
-    compute_ms = min(ev_ms(torch, cs, lambda: [layer() for _ in range(L)]) for _ in range(2))
     d2h_s = dev.torch_stream("d2h")
 
     def prefill_with_offload():
@@ -369,7 +368,12 @@ def prefill_rows(torch, dev_t, link, tf_peak):
         kv.release(0)
         return e0.elapsed_time(e1)
     dev.set_timing(True)  # copy-engine busy time of the D2H copies (CUDA events around each batch)
-    with_ms = min(prefill_with_offload() for _ in range(3))
+    # compute-only and with-offload runs interleaved (clock / power drift hits both), min of 3 each
+    compute_runs, with_runs = [], []
+    for _ in range(3):
+        compute_runs.append(ev_ms(torch, cs, lambda: [layer() for _ in range(L)]))
+        with_runs.append(prefill_with_offload())
+    compute_ms, with_ms = min(compute_runs), min(with_runs)
     ost = dev.offload_stats(reset=True)
     bytes_off = ost.d2h_bytes_algorithmic // 3
     d2h_busy_ms = ost.d2h_ms / 3
@@ -394,7 +398,9 @@ def prefill_rows(torch, dev_t, link, tf_peak):
             "hidden_frac": max(0.0, 1.0 - exposed / link_ms) if link_ms else None,
             "last_layer_offload_at_link_peak_ms": link_ms / L,
             "d2h_busy_ms": d2h_busy_ms, "d2h_gbs_while_busy": bytes_off / (d2h_busy_ms / 1e3) / 1e9 if d2h_busy_ms else None,
-            "timing": "CUDA events: compute stream start -> D2H stream end, min of 3 prefills",
+            "timing": "CUDA events: compute stream start -> D2H stream end; compute-only and with-offload "
+                      "prefills interleaved, min of 3 each",
+            "compute_runs_ms": compute_runs, "with_offload_runs_ms": with_runs,
             "offload_gbs_during_prefill": bytes_off / (with_ms / 1e3) / 1e9,
             "layer_tflops": L * (flops + dense_flops) / compute_ms / 1e9,
             "measured_prefill_ms": with_ms,

@@ -719,23 +719,34 @@ struct lkv_device final : layersim::KvObserver {
           LKV_CUDA(cudaGetLastError());
           ostats.scatter_bytes += (e - b) * sb;
         } else if (where == Loc::Cpu) {
-          for (long long c0 = b; c0 < e; c0 += seg_slots) {
-            const long long cnt = std::min(seg_slots, e - c0);
-            const int seg = next_segment();
-            const long long vecs = cnt * sb / 16;
+          // One pack launch per run of consecutive staging segments (up to the
+          // ring's wrap), then one D2H per segment.
+          long long c0 = b;
+          while (c0 < e) {
+            const long long want = (e - c0 + seg_slots - 1) / seg_slots;
+            const long long nseg = std::min<long long>(want, cfg.staging_chunks - seg_next);
+            const int seg0 = seg_next;
+            for (long long k = 0; k < nseg; ++k) next_segment();
+            const long long cnt_all = std::min(nseg * seg_slots, e - c0);
+            const long long vecs = cnt_all * sb / 16;
             const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
-            scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(c0), static_cast<int>(cnt),
-                                                    nullptr, d_staging + seg * seg_slots * sb, sb, Hl, bs, D);
+            scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(c0), static_cast<int>(cnt_all),
+                                                    nullptr, d_staging + seg0 * seg_slots * sb, sb, Hl, bs, D);
             LKV_CUDA(cudaGetLastError());
-            std::vector<long long> cpu(cnt);
-            for (long long i = 0; i < cnt; ++i) {
-              const auto& en = r.blocks[c0 + i].layers[l];
-              check_slot(en);
-              cpu[i] = en.slot;
+            for (long long k = 0; k < nseg; ++k) {
+              const long long s0 = c0 + k * seg_slots;
+              const long long cnt = std::min(seg_slots, e - s0);
+              std::vector<long long> cpu(cnt);
+              for (long long i = 0; i < cnt; ++i) {
+                const auto& en = r.blocks[s0 + i].layers[l];
+                check_slot(en);
+                cpu[i] = en.slot;
+              }
+              d2h_segment(seg0 + static_cast<int>(k), cpu.data(), cnt);
+              const long long tok_hi = std::min(tokens, (s0 + cnt) * bs);
+              ostats.d2h_bytes_algorithmic += (tok_hi - s0 * bs) * (sb / bs);
             }
-            d2h_segment(seg, cpu.data(), cnt);
-            const long long tok_hi = std::min(tokens, (c0 + cnt) * bs);
-            ostats.d2h_bytes_algorithmic += (tok_hi - c0 * bs) * (sb / bs);
+            c0 += cnt_all;
           }
         }
         b = e;
