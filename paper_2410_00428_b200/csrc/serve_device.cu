@@ -184,10 +184,13 @@ class DeviceExecutor final : public lkv::Executor {
     const float scale = 1.0f / std::sqrt(static_cast<float>(d_));
     SERVE_CUDA(cudaEventRecord(ev0_, cs_));
     for (int l = 0; l < cfg_.model.n_layers; ++l) {
+      // QKV projection -> the layer's K/V exist: pack + D2H them right away so
+      // the copy overlaps this layer's attention and MLP
+      if (o_.dense) qkv_gemm(prompt);
       SERVE_LKV(lkv_fill_kv(dev_, k_, v_, prompt, 0, l, o_.kv_seed, cs_));
-      if (o_.dense) dense(prompt);
-      if (o_.attention) SERVE_LKV(lkv_prefill_attention(dev_, q_, k_, v_, out_, prompt, scale, LKV_DTYPE_BF16, cs_));
       SERVE_LKV(lkv_prefill_layer(dev_, id, l, k_, v_, prompt, cs_));
+      if (o_.attention) SERVE_LKV(lkv_prefill_attention(dev_, q_, k_, v_, out_, prompt, scale, LKV_DTYPE_BF16, cs_));
+      if (o_.dense) rest_gemms(prompt);
       launches_ += 1 + (o_.dense ? 4 : 0) + (o_.attention ? 1 : 0) + 2;  // fill, gemms, attention, table + scatter/pack
     }
     SERVE_CUDA(cudaEventRecord(ev1_, cs_));
@@ -295,11 +298,15 @@ class DeviceExecutor final : public lkv::Executor {
   }
   // The layer's projections and MLP: QKV, O, gate+up, down (norms, RoPE and
   // the SiLU product are elementwise and left out).
-  void dense(std::int64_t M) {
-    gemm(x_, w_, y_, M, qkv_, hid_);
+  void qkv_gemm(std::int64_t M) { gemm(x_, w_, y_, M, qkv_, hid_); }
+  void rest_gemms(std::int64_t M) {  // O projection, gate+up, down
     gemm(x_, w_, y_, M, hid_, hid_);
     gemm(x_, w_, y_, M, 2 * ffn_, hid_);
     gemm(y_, w_, x_, M, hid_, ffn_);
+  }
+  void dense(std::int64_t M) {
+    qkv_gemm(M);
+    rest_gemms(M);
   }
   double span_s() {
     SERVE_CUDA(cudaEventSynchronize(ev1_));
