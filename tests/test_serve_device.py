@@ -33,7 +33,8 @@ def engine_golden():
 
 # te_contended also passes (261 s: 8.3 TB of re-fetches at the link's 55 GB/s); esc_small and
 # te_fcfs_layerkv cover escalations in seconds.
-@pytest.mark.parametrize("name", ["te_fcfs_layerkv", "esc_small", "cfg1_x16", "cfg1_x0", "te_determinism_baseline"])
+@pytest.mark.parametrize("name", ["te_fcfs_layerkv", "esc_small", "cfg1_x16", "cfg1_x0", "te_determinism_baseline",
+                                  "cfg4_tp8"])
 def test_device_virtual_matches_reference_and_bytes(engine_golden, name):
     sc = mg.ENGINE_SCENARIOS[name]
     cfg = serve_cfg(sc, executor="device-virtual", dense_gemms=False, prefill_attention=False, verify_kv=True)
