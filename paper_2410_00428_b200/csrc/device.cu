@@ -558,6 +558,24 @@ struct lkv_device final : layersim::KvObserver {
     return copies;
   }
 
+  // Scatter K/V blocks [b0, b0+n) of a prefill layer into slots: frames =
+  // the layer's table row (GPU slots, absolute block index) or nullptr for a
+  // contiguous destination (staging).
+  void scatter_blocks(const __nv_bfloat16* kb, const __nv_bfloat16* vb, long long tokens, long long b0, long long n,
+                      const int* frames, char* dst) {
+    if (n <= 0) return;
+    if (D == 128 && (bs & (bs - 1)) == 0) {
+      scatter_slots_kernel<<<static_cast<unsigned>(2 * n), 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b0), frames,
+                                                                        dst, sb, Hl, __builtin_ctz(bs));
+    } else {
+      const long long vecs = n * sb / 16;
+      const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
+      scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b0), static_cast<int>(n), frames, dst,
+                                              sb, Hl, bs, D);
+    }
+    LKV_CUDA(cudaGetLastError());
+  }
+
   int next_segment() {
     const int i = seg_next;
     seg_next = (seg_next + 1) % cfg.staging_chunks;
@@ -618,23 +636,31 @@ struct lkv_device final : layersim::KvObserver {
         throw CapacityError("CPU slot " + std::to_string(e.cpu_slot) + " >= host frames");
       tokens += e.filled_tokens;
     }
-    for (long long i0 = 0; i0 < n; i0 += seg_slots) {
-      const long long cnt = std::min(seg_slots, n - i0);
-      const int seg = next_segment();
-      auto* slots = reinterpret_cast<unsigned*>(ring.reserve(cnt * sizeof(unsigned)));
-      std::vector<long long> cpu(cnt);
-      for (long long i = 0; i < cnt; ++i) {
-        slots[i] = entries[i0 + i].gpu_slot;
-        cpu[i] = entries[i0 + i].cpu_slot;
-      }
-      unsigned* dl = d_slotlist + seg * seg_slots;
-      LKV_CUDA(cudaMemcpyAsync(dl, slots, cnt * sizeof(unsigned), cudaMemcpyHostToDevice, cs));
+    // One gather launch per run of consecutive staging segments (up to the
+    // ring's wrap; a CTA per slot), then one D2H per segment.
+    long long i0 = 0;
+    while (i0 < n) {
+      const long long want = (n - i0 + seg_slots - 1) / seg_slots;
+      const long long nseg = std::min<long long>(want, cfg.staging_chunks - seg_next);
+      const int seg0 = seg_next;
+      for (long long k = 0; k < nseg; ++k) next_segment();
+      const long long cnt_all = std::min(nseg * seg_slots, n - i0);
+      auto* slots = reinterpret_cast<unsigned*>(ring.reserve(cnt_all * sizeof(unsigned)));
+      for (long long i = 0; i < cnt_all; ++i) slots[i] = entries[i0 + i].gpu_slot;
+      unsigned* dl = d_slotlist + seg0 * seg_slots;
+      LKV_CUDA(cudaMemcpyAsync(dl, slots, cnt_all * sizeof(unsigned), cudaMemcpyHostToDevice, cs));
       ring.commit(cs);
-      const int grid = static_cast<int>(std::min<long long>(4ll * sms, (cnt * sb / 16 + 255) / 256));
-      gather_slots_kernel<<<std::max(grid, 1), 256, 0, cs>>>(dbuf, dl, static_cast<int>(cnt), sb,
-                                                             d_staging + seg * seg_slots * sb);
+      gather_slots_v2_kernel<<<static_cast<unsigned>(cnt_all), 256, 0, cs>>>(dbuf, dl, sb,
+                                                                              d_staging + seg0 * seg_slots * sb);
       LKV_CUDA(cudaGetLastError());
-      d2h_segment(seg, cpu.data(), cnt);
+      for (long long k = 0; k < nseg; ++k) {
+        const long long s0 = i0 + k * seg_slots;
+        const long long cnt = std::min(seg_slots, n - s0);
+        std::vector<long long> cpu(cnt);
+        for (long long i = 0; i < cnt; ++i) cpu[i] = entries[s0 + i].cpu_slot;
+        d2h_segment(seg0 + static_cast<int>(k), cpu.data(), cnt);
+      }
+      i0 += cnt_all;
     }
     cudaEvent_t ev;
     ev_create(&ev, true);
@@ -698,11 +724,7 @@ struct lkv_device final : layersim::KvObserver {
     const auto* kb = static_cast<const __nv_bfloat16*>(k);
     const auto* vb = static_cast<const __nv_bfloat16*>(v);
     if (n_gpu == nb && nb > 0) {
-      const long long vecs = nb * sb / 16;
-      const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
-      scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, 0, static_cast<int>(nb),
-                                              d_table + tindex(row, l, 0), dbuf, sb, Hl, bs, D);
-      LKV_CUDA(cudaGetLastError());
+      scatter_blocks(kb, vb, tokens, 0, nb, d_table + tindex(row, l, 0), dbuf);
       ostats.scatter_bytes += nb * sb;
     } else {
       // Runs of blocks by residency; GPU runs scatter, CPU runs pack+D2H.
@@ -712,11 +734,7 @@ struct lkv_device final : layersim::KvObserver {
         long long e = b + 1;
         while (e < nb && r.blocks[e].layers[l].loc == where) ++e;
         if (where == Loc::Gpu) {
-          const long long vecs = (e - b) * sb / 16;
-          const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
-          scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b), static_cast<int>(e - b),
-                                                  d_table + tindex(row, l, 0), dbuf, sb, Hl, bs, D);
-          LKV_CUDA(cudaGetLastError());
+          scatter_blocks(kb, vb, tokens, b, e - b, d_table + tindex(row, l, 0), dbuf);
           ostats.scatter_bytes += (e - b) * sb;
         } else if (where == Loc::Cpu) {
           // One pack launch per run of consecutive staging segments (up to the
@@ -728,11 +746,8 @@ struct lkv_device final : layersim::KvObserver {
             const int seg0 = seg_next;
             for (long long k = 0; k < nseg; ++k) next_segment();
             const long long cnt_all = std::min(nseg * seg_slots, e - c0);
-            const long long vecs = cnt_all * sb / 16;
-            const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
-            scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(c0), static_cast<int>(cnt_all),
-                                                    nullptr, d_staging + seg0 * seg_slots * sb, sb, Hl, bs, D);
-            LKV_CUDA(cudaGetLastError());
+            // frames == nullptr: block c0 + i -> staging slot i
+            scatter_blocks(kb, vb, tokens, c0, cnt_all, nullptr, d_staging + seg0 * seg_slots * sb);
             for (long long k = 0; k < nseg; ++k) {
               const long long s0 = c0 + k * seg_slots;
               const long long cnt = std::min(seg_slots, e - s0);

@@ -93,8 +93,71 @@ __global__ void scatter_kv_kernel(const __nv_bfloat16* __restrict__ k,
   }
 }
 
+// One CTA per half slot (K or V of block b0 + i): [Hl][bs][128] bf16, written
+// contiguously; source rows (token, head) of the prefill K/V. 32-bit index
+// math (bs = 1 << bs_shift, D = 128) and 4 independent 16 B loads in flight
+// per thread. Replaces the grid-stride scatter_kv_kernel on the hot path
+// (which spent its issue slots on 64-bit div/mod).
+__global__ void __launch_bounds__(256) scatter_slots_kernel(const __nv_bfloat16* __restrict__ k,
+                                                            const __nv_bfloat16* __restrict__ v, long long tokens,
+                                                            int b0, const int* __restrict__ frames,
+                                                            char* __restrict__ dst, long long slot_bytes, int Hl,
+                                                            int bs_shift) {
+  const int half = static_cast<int>(blockIdx.x & 1u);
+  const int bl = static_cast<int>(blockIdx.x >> 1);
+  const int b = b0 + bl;
+  const long long frame = frames ? frames[b] : bl;
+  char* out = dst + frame * slot_bytes + half * (slot_bytes >> 1);
+  const __nv_bfloat16* src = half ? v : k;
+  const int bs_mask = (1 << bs_shift) - 1;
+  const int nvec = (Hl << bs_shift) << 4;  // 16 vectors of 8 bf16 per (head, token) row
+  const long long tok0 = static_cast<long long>(b) << bs_shift;
+  for (int j0 = threadIdx.x; j0 < nvec; j0 += 4 * blockDim.x) {
+    uint4 val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * blockDim.x;
+      val[u] = make_uint4(0, 0, 0, 0);
+      if (j < nvec) {
+        const int c = j & 15, row = j >> 4;
+        const long long tok = tok0 + (row & bs_mask);
+        if (tok < tokens) val[u] = ld_stream(src + ((tok * Hl + (row >> bs_shift)) << 7) + c * 8);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * blockDim.x;
+      if (j < nvec) st_stream(out + static_cast<long long>(j) * 16, val[u]);
+    }
+  }
+}
+
+// One CTA per slot: pool slot slots[i] -> dst + i * slot_bytes (the
+// escalation gather into staging), 4 x 16 B loads in flight per thread.
+__global__ void __launch_bounds__(256) gather_slots_v2_kernel(const char* __restrict__ pool,
+                                                              const unsigned* __restrict__ slots,
+                                                              long long slot_bytes, char* __restrict__ dst) {
+  const char* src = pool + static_cast<long long>(slots[blockIdx.x]) * slot_bytes;
+  char* out = dst + static_cast<long long>(blockIdx.x) * slot_bytes;
+  const int nvec = static_cast<int>(slot_bytes >> 4);
+  for (int j0 = threadIdx.x; j0 < nvec; j0 += 4 * blockDim.x) {
+    uint4 val[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * blockDim.x;
+      if (j < nvec) val[u] = ld_stream(src + static_cast<long long>(j) * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * blockDim.x;
+      if (j < nvec) st_stream(out + static_cast<long long>(j) * 16, val[u]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
-// Gather: whole slots (list) -> contiguous staging, in list order.
+// Gather: whole slots (list) -> contiguous staging, in list order (grid-stride
+// form, kept for reference; the path launches gather_slots_v2_kernel).
 __global__ void gather_slots_kernel(const char* __restrict__ pool, const unsigned* __restrict__ slots,
                                     int n, long long slot_bytes, char* __restrict__ dst) {
   const long long vec_per_slot = slot_bytes / 16;
