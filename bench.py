@@ -524,6 +524,53 @@ def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=
             "timing": "wall clock around decode_begin..synchronize (host read-ins are on the critical path)"}
 
 
+def scatter_gather_row(torch, dev_t, hbm_peak, T=16384, L=4):
+    """a6/a14 scatter (a retained prefill layer's K/V into its GPU slots) and
+    a8/a15 escalation gather (a request's GPU slots into staging ahead of the
+    D2H), 7B shape (32 KV heads, bs 16, 256 KiB slots). CUDA events on the
+    compute stream around lkv_prefill_layer / plan_offload; algorithmic bytes
+    = read + write of every slot byte."""
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import Device, DeviceConfig
+    bs = 16
+    model = ls.ModelSpec(L, 32, 32, 128, 4096, 7e9, 2)
+    nblk = T // bs
+    kv = ls.KvManager(ls.BlockPools(nblk * L + 64, nblk * L + 64, bs), model)
+    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=nblk * L + 64,
+                                             host_slots=nblk * L + 64, arena_slots=64, max_requests=4,
+                                             max_blocks=nblk + 4, max_batch=2, staging_chunks=64, chunk_bytes=16 << 20))
+    cs = dev.torch_stream("compute")
+    k = torch.empty((T, 32, 128), dtype=torch.bfloat16, device=dev_t)
+    v = torch.empty_like(k)
+    dev.fill_kv(k, v, T, 0, 0, SEED, stream=cs)
+    slot_bytes = dev.slot_bytes
+    best_s = best_g = None
+    for _ in range(3):
+        assert kv.allocate_prefill(0, T, L)  # every layer retained: scatter only
+        torch.cuda.synchronize()
+        e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        e0.record(cs)
+        for layer in range(L):
+            dev.prefill_layer(0, layer, k, v, T, stream=cs)
+        e1.record(cs)
+        job = kv.plan_offload(0, ls.FULL)  # gather of all L x nblk GPU slots into staging (+ D2H on its stream)
+        e2.record(cs)
+        dev.synchronize()
+        kv.complete_offload(job.job_id)
+        kv.release(0)
+        s_ms, g_ms = e0.elapsed_time(e1), e1.elapsed_time(e2)
+        best_s = s_ms if best_s is None else min(best_s, s_ms)
+        best_g = g_ms if best_g is None else min(best_g, g_ms)
+    dev.close()
+    byts = 2 * L * nblk * slot_bytes
+    return {"workload": f"7B shape, {T} tokens x {L} layers, 256 KiB slots",
+            "scatter": {"kernel": "scatter_slots_kernel", "ms": best_s, "gbs": byts / (best_s / 1e3) / 1e9,
+                        "frac": byts / (best_s / 1e3) / 1e9 / hbm_peak},
+            "gather": {"kernel": "gather_slots_v2_kernel", "ms": best_g, "gbs": byts / (best_g / 1e3) / 1e9,
+                       "frac": byts / (best_g / 1e3) / 1e9 / hbm_peak},
+            "ncu": "profiles/r1w_scatter_gather_ncu.txt"}
+
+
 def serving_row(link, tf_peak, hbm_peak, n=6, prompt=16384, output=8, rate=8.0):
     """f1: the product's serving loop on config 2's shape (7B, 48 GB-capped
     pools, LayerKV policy, fixed 16k prompts arriving fast enough to force
@@ -768,6 +815,7 @@ def main():
             rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak)
             rows["a18_gqa_decode_70b_tp8_shard"] = gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8, tp_size=8,
                                                                   B=64, ctx=32768, label="70B GQA TP8 rank 0")
+            rows["a6_a8_scatter_gather"] = scatter_gather_row(torch, dev_t, hbm_peak)
             rows["f1_measured_serving"] = serving_row(link, tensor_peak(), hbm_peak)
             rows["f3_tiered_host_decode"] = tiered_host_row(torch, dev_t, link)
             line["rows"] = rows
