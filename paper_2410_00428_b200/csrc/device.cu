@@ -420,8 +420,32 @@ struct lkv_device final : layersim::KvObserver {
                           std::to_string(cfg.host_slots));
   }
 
+  // The journal may update one table entry several times before a flush
+  // (e.g. complete_offload rewrites a row, release frees it, allocate_prefill
+  // hands it to the next request). table_apply_kernel writes in parallel, so
+  // only the last update per entry is kept (in journal order).
+  std::unordered_map<long long, std::size_t> journal_last;
+  void dedupe_journal() {
+    journal_last.clear();
+    journal_last.reserve(journal.size() * 2);
+    bool dup = false;
+    for (std::size_t i = 0; i < journal.size(); ++i) {
+      auto [it, fresh] = journal_last.try_emplace(journal[i].index, i);
+      if (!fresh) {
+        it->second = i;
+        dup = true;
+      }
+    }
+    if (!dup) return;
+    std::size_t w = 0;
+    for (std::size_t i = 0; i < journal.size(); ++i)
+      if (journal_last[journal[i].index] == i) journal[w++] = journal[i];
+    journal.resize(w);
+  }
+
   void flush() {
     if (journal.empty()) return;
+    dedupe_journal();
     const std::size_t n = journal.size();
     auto* dst = reinterpret_cast<TableUpdate*>(ring.reserve(n * sizeof(TableUpdate)));
     std::memcpy(dst, journal.data(), n * sizeof(TableUpdate));

@@ -208,3 +208,20 @@ def test_default_stream_inputs_are_ordered():
     got = out[0].cpu().numpy()
     err = np.abs(got - want).max(axis=-1) / np.abs(want).max(axis=-1)
     assert err.max() <= sc.REL_TOL
+
+
+def test_table_journal_last_update_wins():
+    """complete_offload, release and the next allocate_prefill can rewrite the
+    same table entries before one flush; the device table must end with the
+    last value (regression: the parallel apply raced on duplicate entries
+    and a scatter went to a stale CPU-slot frame)."""
+    model = sc.gqa_model(L=4, hkv=8, group=1)
+    kv, dev = sc.make(model, gpu=3000, cpu=3000, max_blocks=200)
+    for it in range(6):
+        sc.prefill(kv, dev, 0, 1500, 4)  # every layer retained: scatter through the table row
+        assert dev.verify_request(0, 1500, sc.SEED) == 0, f"iteration {it}"
+        job = kv.plan_offload(0, ls.FULL)
+        dev.synchronize()
+        kv.complete_offload(job.job_id)  # journal: every entry -> its CPU slot
+        kv.release(0)                    # the row returns to the free list, same row next time
+    dev.close()
