@@ -258,7 +258,7 @@ def workload_config(args):
             "l2": "inputs larger than L2 (one layer's KV = 1.88 GB)",
             "parallelism": f"kv-head tp{args.gpus}", "pipeline_depth": args.depth,
             "allgather": (None if args.gpus == 1 else
-                          "fused into decode_merge_v4_kernel (NVLink peer stores + epoch flags)" if args.allgather == "fused"
+                          "fused into decode_merge_v5_kernel (NVLink peer stores + epoch flags)" if args.allgather == "fused"
                           else "NCCL all_gather_into_tensor")}
 
 
@@ -794,7 +794,7 @@ def main():
                          "frac": achieved / hbm_peak, "traffic": traffic,
                          "kernel": "decode_attn_v2_kernel<G=1>", "peak_kind": peak_kind,
                          "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms,
-                         "split_merge": {"kernel": "decode_merge_v4_kernel", "avg_launch_ms":
+                         "split_merge": {"kernel": "decode_merge_v5_kernel", "avg_launch_ms":
                                          merge_ms / max(attn_launches, 1),
                                          "attention_plus_merge_frac": per_launch_bytes / (
                                              (avg_launch_ms + merge_ms / max(attn_launches, 1)) / 1000) / 1e9 / hbm_peak}},

@@ -418,6 +418,133 @@ __global__ void gather_wait_kernel(const unsigned* __restrict__ flags, int n, un
   __syncwarp();
 }
 
+// Writes merged row (member m, query head hq): lane owns dims 4*lane..+3.
+// Also stores the row into every rank's gather buffer and, from the launch's
+// last CTA, publishes the epoch (fused all-gather). Called by
+// all threads of the CTA; warp 0 holds the row.
+__device__ __forceinline__ void merge_store_row(float4 r, float Lt, int m, int hq, int Hl, int G, void* out,
+                                                int out_f32, const GatherArgs& ga) {
+  if ((threadIdx.x >> 5) == 0) {
+    const int lane = threadIdx.x & 31;
+    const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
+    const long long idx = (static_cast<long long>(m) * Hl * G + hq) * kHeadDim + lane * 4;
+    uint2 pk;
+    pk.x = (static_cast<unsigned>(__bfloat16_as_ushort(__float2bfloat16_rn(r.y * inv))) << 16) |
+           __bfloat16_as_ushort(__float2bfloat16_rn(r.x * inv));
+    pk.y = (static_cast<unsigned>(__bfloat16_as_ushort(__float2bfloat16_rn(r.w * inv))) << 16) |
+           __bfloat16_as_ushort(__float2bfloat16_rn(r.z * inv));
+    if (out_f32)
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + idx) = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
+    else
+      *reinterpret_cast<uint2*>(static_cast<__nv_bfloat16*>(out) + idx) = pk;
+    if (ga.bases) {  // this row into every rank's gather buffer (NVLink stores to peers)
+      const long long row = (static_cast<long long>(ga.parity) * ga.max_batch + m) * ga.hq_total +
+                            static_cast<long long>(ga.rank) * Hl * G + hq;
+      const long long off = kGatherFlagWords * 4 + row * kHeadDim * 2 + lane * 8;
+      for (int p = 0; p < ga.n; ++p) *reinterpret_cast<uint2*>(ga.bases[p] + off) = pk;
+    }
+  }
+  if (ga.bases) {  // the launch's last CTA publishes the epoch to every rank
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned total = gridDim.x * gridDim.y;
+      if (atomicAdd(ga.done, 1u) == total - 1) {
+        __threadfence_system();
+        for (int p = 0; p < ga.n; ++p)
+          st_release_sys(reinterpret_cast<unsigned*>(ga.bases[p]) + ga.rank, ga.epoch);
+        *ga.done = 0u;
+      }
+    }
+  }
+}
+
+// Merge v5: one CTA (8 warps) per (member, query head), a single pass. Warp w
+// folds chunks w, w+8, ... in batches of 8 with every load of a batch issued
+// before any math, and keeps its own running max (rescaling its sum when a
+// batch raises it), so no separate max pass costs a memory round trip; the
+// eight (max, sum, row) partials meet in shared memory. 64 loads of 512 B in
+// flight per CTA: the merge is latency-bound (few CTAs, L2-resident partials).
+__global__ void __launch_bounds__(256) decode_merge_v5_kernel(const float* __restrict__ part_o,
+                                                              const float* __restrict__ part_ml,
+                                                              const AttnSeq* __restrict__ seqs, int Hl, int G,
+                                                              void* __restrict__ out, int out_f32,
+                                                              GatherArgs ga) {
+  constexpr int W = 8, B = 8;
+  __shared__ float4 so[W][32];
+  __shared__ float sm_[W], sl_[W];
+  const int m = blockIdx.x, hq = blockIdx.y, h = hq / G, g = hq % G;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const AttnSeq sd = seqs[m];
+  const int nch = sd.nchunk;
+  const long long cstride = static_cast<long long>(Hl) * G;
+  const long long pu0 = (static_cast<long long>(sd.chunk0) * Hl + h) * G + g;
+  float M = -INFINITY, L = 0.f;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c0 = warp; c0 < nch; c0 += W * B) {
+    float4 v[B];
+    float2 ml[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const int c = c0 + W * i;
+      if (c < nch) {
+        const long long pu = pu0 + c * cstride;
+        v[i] = __ldcg(reinterpret_cast<const float4*>(part_o + pu * kHeadDim) + lane);
+        ml[i] = __ldcg(reinterpret_cast<const float2*>(part_ml + pu * 2));
+      } else {
+        v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+        ml[i] = make_float2(-INFINITY, 0.f);
+      }
+    }
+    float mb = M;
+#pragma unroll
+    for (int i = 0; i < B; ++i) mb = fmaxf(mb, ml[i].x);
+    if (mb == -INFINITY) continue;  // nothing valid yet
+    const float cs = (M == -INFINITY) ? 0.f : exp2f(M - mb);
+    L *= cs;
+    acc.x *= cs;
+    acc.y *= cs;
+    acc.z *= cs;
+    acc.w *= cs;
+    M = mb;
+#pragma unroll
+    for (int i = 0; i < B; ++i) {
+      const float f = (ml[i].x == -INFINITY) ? 0.f : exp2f(ml[i].x - M);
+      L = fmaf(f, ml[i].y, L);
+      acc.x = fmaf(f, v[i].x, acc.x);
+      acc.y = fmaf(f, v[i].y, acc.y);
+      acc.z = fmaf(f, v[i].z, acc.z);
+      acc.w = fmaf(f, v[i].w, acc.w);
+    }
+  }
+  so[warp][lane] = acc;
+  if (lane == 0) {
+    sm_[warp] = M;
+    sl_[warp] = L;
+  }
+  __syncthreads();
+  float4 r = make_float4(0.f, 0.f, 0.f, 0.f);
+  float Lt = 0.f;
+  if (warp == 0) {
+    float Mg = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < W; ++w) Mg = fmaxf(Mg, sm_[w]);
+    if (Mg != -INFINITY) {
+#pragma unroll
+      for (int w = 0; w < W; ++w) {
+        const float f = (sm_[w] == -INFINITY) ? 0.f : exp2f(sm_[w] - Mg);
+        const float4 a = so[w][lane];
+        Lt = fmaf(f, sl_[w], Lt);
+        r.x = fmaf(f, a.x, r.x);
+        r.y = fmaf(f, a.y, r.y);
+        r.z = fmaf(f, a.z, r.z);
+        r.w = fmaf(f, a.w, r.w);
+      }
+    }
+  }
+  merge_store_row(r, Lt, m, hq, Hl, G, out, out_f32, ga);
+}
+
 // One CTA (4 warps) per (member, query head). Every warp finds the global max
 // over the chunks (lanes stride over chunks), then warp w folds chunks w,
 // w+4, ... with all its o-row loads issued before any FMA (8 in flight per

@@ -60,6 +60,27 @@ __device__ __forceinline__ void named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// Named barrier that also ORs a predicate over its n threads.
+__device__ __forceinline__ bool named_bar_or(int id, int n, bool v) {
+  uint32_t r;
+  asm volatile(
+      "{\n"
+      ".reg .pred p, q;\n"
+      "setp.ne.u32 p, %1, 0;\n"
+      "bar.red.or.pred q, %2, %3, p;\n"
+      "selp.u32 %0, 1, 0, q;\n"
+      "}\n"
+      : "=r"(r)
+      : "r"(static_cast<uint32_t>(v)), "r"(id), "r"(n)
+      : "memory");
+  return r != 0;
+}
+
+// Lazy running max (log2 domain): a tile rescales only when one of its scores
+// exceeds the running max of its head by more than this (exp2 <= 2^8 keeps P
+// and the fp32 sums far from overflow), so most tiles skip the max reduction.
+constexpr float kLazyMax = 8.f;
+
 template <int G, int BS, int NS>
 __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
     const __grid_constant__ CUtensorMap kvmap, int Hl, const int* __restrict__ snap,
@@ -196,9 +217,30 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const AttnChunk ck = chunks[u / Hl];
         const int ntile = (ck.nb + TB - 1) / TB;
+        if (have_prev) {  // same for the previous unit's last PV while this unit's Q loads
+          while (!tc::bar_test(&q_full[qb], qph)) {
+            if (tc::bar_test(&p_full[prev_j & 1], (prev_j >> 1) & 1u)) {
+              issue_pv(prev_stage, prev_j);
+              have_prev = false;
+              break;
+            }
+          }
+        }
         tc::bar_wait(&q_full[qb], qph);
         for (int t = 0; t < ntile; ++t) {
           const int sb = j & 1;
+          // PV(j-1) frees its K/V stage for the producer: issue it as soon as
+          // P(j-1) is ready instead of behind the arrival of tile j, so a late
+          // tile never holds a finished stage (one more stage of loads in flight).
+          if (have_prev) {
+            while (!tc::bar_test(&full[stage], ph)) {
+              if (tc::bar_test(&p_full[prev_j & 1], (prev_j >> 1) & 1u)) {
+                issue_pv(prev_stage, prev_j);
+                have_prev = false;
+                break;
+              }
+            }
+          }
           tc::bar_wait(&full[stage], ph);
           tc::bar_wait(&s_empty[sb], ((j >> 1) & 1u) ^ 1u);
           tc::fence_after_sync();
@@ -269,29 +311,42 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
         const int bi = t * TB + r / BS;
         const int tok = (ck.b0 + bi) * BS + (r % BS);
         const bool valid = bi < ck.nb && tok < kv_len;
-        float* rd = red + (j & 1) * 32;
+        bool raise = false;
 #pragma unroll
         for (int g = 0; g < G; ++g) {
           s[g] = valid ? s[g] * scale_log2 : -INFINITY;
-          float mx = s[g];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          if (lane == 0) rd[quad * 8 + g] = mx;
+          raise |= s[g] > m_run[g] + kLazyMax;  // -inf running max: any valid score raises
         }
-        named_bar_sync(1, 128);
         float corr[G];
-        uint32_t hi[4], lo[4];
         float p[8];
 #pragma unroll
         for (int g = 0; g < 8; ++g) p[g] = 0.f;
+        if (named_bar_or(1, 128, raise)) {  // uniform: some head's max moved too far, reduce exactly
+          float* rd = red + (j & 1) * 32;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            float mx = s[g];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            if (lane == 0) rd[quad * 8 + g] = mx;
+          }
+          named_bar_sync(1, 128);
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const float tmax = fmaxf(fmaxf(rd[g], rd[8 + g]), fmaxf(rd[16 + g], rd[24 + g]));
+            const float mnew = fmaxf(m_run[g], tmax);
+            corr[g] = (m_run[g] == -INFINITY) ? 0.f : exp2f(m_run[g] - mnew);
+            m_run[g] = mnew;
+          }
+        } else {
+#pragma unroll
+          for (int g = 0; g < G; ++g) corr[g] = 1.f;
+        }
+        uint32_t hi[4], lo[4];
 #pragma unroll
         for (int g = 0; g < G; ++g) {
-          const float tmax = fmaxf(fmaxf(rd[g], rd[8 + g]), fmaxf(rd[16 + g], rd[24 + g]));
-          const float mnew = fmaxf(m_run[g], tmax);
-          corr[g] = (m_run[g] == -INFINITY) ? 0.f : exp2f(m_run[g] - mnew);
-          p[g] = (s[g] == -INFINITY) ? 0.f : exp2f(s[g] - mnew);
+          p[g] = (s[g] == -INFINITY) ? 0.f : exp2f(s[g] - m_run[g]);
           l_part[g] = fmaf(l_part[g], corr[g], p[g]);
-          m_run[g] = mnew;
         }
         // P = hi + lo, both bf16 (columns g and 8+g of the N=16 operand): the
         // PV product keeps ~16 mantissa bits of P at no extra MMA cost, which

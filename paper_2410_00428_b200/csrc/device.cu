@@ -174,7 +174,7 @@ struct lkv_device final : layersim::KvObserver {
   std::size_t vh_cap = 0;
   cudaEvent_t vh_free = nullptr;
   bool vh_used = false;
-  int merge_version = 4;           // LKV_MERGE=2 / 3: earlier merge kernels (thread = dim / warp per head)
+  int merge_version = 5;           // LKV_MERGE=2 / 3 / 4: earlier merge kernels (thread = dim / warp per head / two-pass 4 warps)
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
@@ -290,7 +290,7 @@ struct lkv_device final : layersim::KvObserver {
     }
     if (const char* mv = std::getenv("LKV_MERGE")) {
       const int v = std::atoi(mv);
-      merge_version = (v == 2 || v == 3) ? v : 4;
+      merge_version = (v >= 2 && v <= 4) ? v : 5;
     }
     {
       const unsigned long long rows = static_cast<unsigned long long>(std::max<long long>(frames, 1)) * 2 * Hl * bs;
@@ -1179,13 +1179,16 @@ struct lkv_device final : layersim::KvObserver {
       }
       if (timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attention kernel | merge kernel
       // merge (members without KV get zero rows: no chunks, L = 0)
-      if (gather_on() && merge_version != 4) throw std::invalid_argument("fused gather needs merge v4");
+      if (gather_on() && merge_version < 4) throw std::invalid_argument("fused gather needs merge v4/v5");
       if (merge_version == 2)
         decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
       else if (merge_version == 3)
         decode_merge_v3_kernel<<<(n * Hql + 3) / 4, 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, n, Hl, G, out, f32);
-      else
+      else if (merge_version == 4)
         decode_merge_v4_kernel<<<dim3(n, Hql), 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32,
+                                                             gather_args(l));
+      else
+        decode_merge_v5_kernel<<<dim3(n, Hql), 256, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32,
                                                              gather_args(l));
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;

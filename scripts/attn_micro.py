@@ -57,7 +57,8 @@ def main():
             kres.append(st.attn_ms / st.attn_launches)
     kvb = a.batch * a.ctx * 2 * hkv * 128 * 2
     ms = min(res)
-    print(json.dumps({"variant": os.environ.get("LKV_V2_CFG", "default"), "group": a.group, "bs": a.bs,
+    print(json.dumps({"variant": os.environ.get("LKV_V2_CFG", "default"), "merge": os.environ.get("LKV_MERGE", "5"),
+                      "group": a.group, "hkv": hkv, "batch": a.batch, "ctx": a.ctx, "bs": a.bs,
                       "ms_per_layer": ms, "kernel_ms": min(kres), "GBps": kvb / (ms / 1e3) / 1e9,
                       "kernel_frac_of_6536.7": kvb / (min(kres) / 1e3) / 1e9 / 6536.7,
                       "frac_of_6536.7": kvb / (ms / 1e3) / 1e9 / 6536.7}))

@@ -107,6 +107,21 @@ def test_attention_parity_each_kernel(kernel, group, bs, monkeypatch):
     sc.check_attention(dev, list(range(len(lens))), lens)
 
 
+@pytest.mark.parametrize("merge", [3, 4, 5])
+@pytest.mark.parametrize("group", [1, 8])
+def test_attention_parity_each_merge(merge, group, monkeypatch):
+    """Every split merge (warp per head, two-pass 4 warps, single-pass 8
+    warps with per-warp running max) on members with 1 to ~300 chunks, so
+    batches cross the running-max rescale and warps see empty chunk lists."""
+    monkeypatch.setenv("LKV_MERGE", str(merge))
+    model = sc.gqa_model(L=2, hkv=2, group=group)
+    kv, dev = sc.make(model, gpu=9000, cpu=9000, max_blocks=4096, arena=9000)
+    lens = [1, 40, 3000, 40000]
+    for rid, n in enumerate(lens):
+        sc.prefill(kv, dev, rid, n, rid % 3)
+    sc.check_attention(dev, list(range(len(lens))), lens)
+
+
 def test_attention_bf16_output():
     model = sc.gqa_model(L=2, hkv=8, group=4)
     kv, dev = sc.make(model)
