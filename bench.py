@@ -461,7 +461,7 @@ def gqa_decode_row(torch, dev_t, hbm_peak, hq=32, hkv=8, tp_size=1, B=16, ctx=32
     q = torch.randn((B, dev.q_heads_local, 128), dtype=torch.bfloat16, device=dev_t)
     out = torch.empty_like(q)
     dev.set_timing(True)
-    best = merge = None
+    best = None
     for it in range(4):
         dev.decode_begin(ids)
         for layer in range(Lr):
@@ -469,16 +469,17 @@ def gqa_decode_row(torch, dev_t, hbm_peak, hq=32, hkv=8, tp_size=1, B=16, ctx=32
         dev.decode_end()
         st = dev.decode_stats()
         if it >= 1:
-            ms = st.attn_ms / st.attn_launches
-            if best is None or ms < best:
-                best, merge = ms, st.merge_ms / st.attn_launches
+            ms = (st.attn_ms + st.merge_ms) / st.attn_launches
+            best = ms if best is None else min(best, ms)
     byts = B * ctx * ls.kv_bytes_per_token_layer(model) // tp_size
     dev.close()
-    return {"kernel": f"decode_gqa_tc_kernel (tcgen05, G={hq // hkv}) + merge",
+    return {"kernel": f"decode_gqa_tc_kernel (tcgen05, G={hq // hkv}) + decode_merge_v5_kernel",
+            "timed_as": "CUDA events around the attention kernel and its PDL-launched split merge together",
             "shape": f"{label} batch {B} x {ctx}, kv heads on this GPU {hkv // tp_size}",
             "ms_per_layer": best, "gbs": byts / (best / 1e3) / 1e9, "peak": hbm_peak,
-            "frac": byts / (best / 1e3) / 1e9 / hbm_peak, "merge_ms_per_layer": merge,
-            "frac_with_merge": byts / ((best + merge) / 1e3) / 1e9 / hbm_peak}
+            "frac": byts / (best / 1e3) / 1e9 / hbm_peak,
+            "frac_of_nominal_8000": byts / (best / 1e3) / 1e9 / 8000.0,
+            "note": "peak is the measured copy (read+write) bandwidth; a read-only KV stream can exceed it"}
 
 
 def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=3):
@@ -792,12 +793,11 @@ def main():
             "config": workload_config(args),
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                          "frac": achieved / hbm_peak, "traffic": traffic,
-                         "kernel": "decode_attn_v2_kernel<G=1>", "peak_kind": peak_kind,
-                         "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms,
-                         "split_merge": {"kernel": "decode_merge_v5_kernel", "avg_launch_ms":
-                                         merge_ms / max(attn_launches, 1),
-                                         "attention_plus_merge_frac": per_launch_bytes / (
-                                             (avg_launch_ms + merge_ms / max(attn_launches, 1)) / 1000) / 1e9 / hbm_peak}},
+                         "kernel": "decode_attn_v2_kernel<G=1> + decode_merge_v5_kernel",
+                         "timed_as": "one CUDA-event interval per layer around the attention kernel and its split "
+                                     "merge (launched as a programmatic dependent, no event between them)",
+                         "peak_kind": peak_kind,
+                         "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms},
             "host_link": {"prefetch_gbs_per_gpu": h2d_alg / world / (h2d_ms / 1000) / 1e9 if h2d_ms else None,
                           "prefetch_algorithmic_bytes_per_step": h2d_alg // args.steps * world,
                           "prefetch_physical_bytes_per_step": h2d_phys // args.steps * world,
@@ -823,7 +823,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_rows:  # §8 rows beside the headline (own devices, after this one is gone)
             rows = prefill_rows(torch, dev_t, link, tensor_peak())
-            rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak)
+            rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak, B=64, label="config 3, 8B GQA")
             rows["a18_gqa_decode_70b_tp8_shard"] = gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8, tp_size=8,
                                                                   B=64, ctx=32768, label="70B GQA TP8 rank 0")
             rows["a6_a8_scatter_gather"] = scatter_gather_row(torch, dev_t, hbm_peak)

@@ -360,11 +360,12 @@ typedef struct lkv_decode_stats {
   int64_t kv_bytes_read;         /* token-exact K+V bytes the attention consumed */
   int64_t attn_launches;
   int64_t kernel_launches;       /* every kernel this iteration launched (snapshot, attention, merge) */
-  double attn_ms;                /* summed CUDA-event time of the attention kernel launches */
+  double attn_ms;                /* summed CUDA-event time of the attention launches: the attention kernel
+                                    plus its PDL-overlapped split merge (LKV_SPLIT_TIMING=1: kernel alone) */
   double h2d_ms;                 /* copy-engine busy time: summed CUDA-event time of each layer's prefetch copies */
   double iteration_ms;           /* decode_begin -> decode_end on the device */
   double h2d_span_ms;            /* first prefetch copy start -> last prefetch copy end */
-  double merge_ms;               /* summed CUDA-event time of the split-merge launches */
+  double merge_ms;               /* split-merge time when LKV_SPLIT_TIMING=1, else 0 (inside attn_ms) */
 } lkv_decode_stats;
 LKV_API int lkv_device_set_timing(lkv_device* dev, int32_t on);
 LKV_API int lkv_decode_last_stats(const lkv_device* dev, lkv_decode_stats* out);

@@ -43,6 +43,15 @@ struct AttnSeq {
   int nchunk;
 };
 
+// Programmatic dependent launch: the attention kernels let the split merge
+// launch early (its CTAs are dispatched next to the persistent attention CTAs
+// and park in griddepcontrol.wait until the attention grid has completed and
+// flushed), so the merge's launch latency hides under the attention kernel.
+__device__ __forceinline__ void pdl_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -194,6 +203,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_attn_v2_kernel(
   }
   __syncwarp();
 
+  pdl_launch_dependents();
   const int gw = blockIdx.x * W + warp;
   const int NW = gridDim.x * W;
   const long long tile_bytes = static_cast<long long>(BS) * D * 2;
@@ -459,20 +469,24 @@ __device__ __forceinline__ void merge_store_row(float4 r, float Lt, int m, int h
   }
 }
 
-// Merge v5: one CTA (8 warps) per (member, query head), a single pass. Warp w
-// folds chunks w, w+8, ... in batches of 8 with every load of a batch issued
+// Merge v5: one CTA (W warps) per (member, query head), a single pass. Warp w
+// folds chunks w, w+W, ... in batches of 8 with every load of a batch issued
 // before any math, and keeps its own running max (rescaling its sum when a
 // batch raises it), so no separate max pass costs a memory round trip; the
-// eight (max, sum, row) partials meet in shared memory. 64 loads of 512 B in
+// W (max, sum, row) partials meet in shared memory. 8W loads of 512 B in
 // flight per CTA: the merge is latency-bound (few CTAs, L2-resident partials).
-__global__ void __launch_bounds__(256) decode_merge_v5_kernel(const float* __restrict__ part_o,
-                                                              const float* __restrict__ part_ml,
-                                                              const AttnSeq* __restrict__ seqs, int Hl, int G,
-                                                              void* __restrict__ out, int out_f32,
-                                                              GatherArgs ga) {
-  constexpr int W = 8, B = 8;
+// W=4 (~110 registers x 128 threads) fits beside a persistent attention CTA,
+// which is what programmatic dependent launch needs to overlap the two.
+template <int W>
+__global__ void __launch_bounds__(W * 32) decode_merge_v5_kernel(const float* __restrict__ part_o,
+                                                               const float* __restrict__ part_ml,
+                                                               const AttnSeq* __restrict__ seqs, int Hl, int G,
+                                                               void* __restrict__ out, int out_f32,
+                                                               GatherArgs ga) {
+  constexpr int B = 8;
   __shared__ float4 so[W][32];
   __shared__ float sm_[W], sl_[W];
+  pdl_wait();  // partials of the attention grid (no-op without PDL)
   const int m = blockIdx.x, hq = blockIdx.y, h = hq / G, g = hq % G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const AttnSeq sd = seqs[m];

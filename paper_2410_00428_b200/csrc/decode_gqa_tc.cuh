@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
   const int rows_per_frame = 2 * Hl * BS;
+  pdl_launch_dependents();
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer

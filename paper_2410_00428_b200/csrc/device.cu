@@ -174,6 +174,13 @@ struct lkv_device final : layersim::KvObserver {
   std::size_t vh_cap = 0;
   cudaEvent_t vh_free = nullptr;
   bool vh_used = false;
+  bool pdl = true;                 // LKV_PDL=0: merge launched without programmatic dependent launch
+  // LKV_SPLIT_TIMING=1: an event between attention and merge, so attn_ms and
+  // merge_ms are separate. Off by default: with the host link saturated by the
+  // prefetch, that event alone adds ~20 us per layer and it defeats PDL, so
+  // attn_ms covers the attention + merge pair and merge_ms stays 0.
+  bool split_timing = false;
+  int merge_warps = 4;             // LKV_MERGE_WARPS=8: wider merge CTA (does not fit beside an attention CTA)
   int merge_version = 5;           // LKV_MERGE=2 / 3 / 4: earlier merge kernels (thread = dim / warp per head / two-pass 4 warps)
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
@@ -288,6 +295,9 @@ struct lkv_device final : layersim::KvObserver {
       const int v = std::atoi(kv);
       kernel_version = (v == 1 || v == 3) ? v : 2;
     }
+    if (const char* e = std::getenv("LKV_PDL")) pdl = std::atoi(e) != 0;
+    if (const char* e = std::getenv("LKV_MERGE_WARPS")) merge_warps = std::atoi(e) == 8 ? 8 : 4;
+    if (const char* e = std::getenv("LKV_SPLIT_TIMING")) split_timing = std::atoi(e) != 0;
     if (const char* mv = std::getenv("LKV_MERGE")) {
       const int v = std::atoi(mv);
       merge_version = (v >= 2 && v <= 4) ? v : 5;
@@ -1145,6 +1155,24 @@ struct lkv_device final : layersim::KvObserver {
     layer_epoch.assign(L, 0);
   }
 
+  // Merge v5 launched as a programmatic dependent of the attention kernel
+  // (LKV_PDL=0 turns it into a plain stream-ordered launch).
+  void launch_merge_v5(int n, void* out, int f32, GatherArgs ga) {
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(n, Hql);
+    lc.blockDim = dim3(merge_warps * 32);
+    lc.dynamicSmemBytes = 0;
+    lc.stream = cs;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = pdl ? 1 : 0;
+    LKV_CUDA(cudaLaunchKernelEx(&lc, merge_warps == 8 ? decode_merge_v5_kernel<8> : decode_merge_v5_kernel<4>, static_cast<const float*>(d_part_o),
+                                static_cast<const float*>(d_part_ml), static_cast<const AttnSeq*>(d_aseqs), Hl, G,
+                                out, f32, ga));
+  }
+
   void decode_layer(int l, const void* q, void* out, float scale, int f32, cudaStream_t user) {
     if (!in_iteration) throw layersim::SimulationError("decode_layer outside decode_begin/end");
     check_layer(l);
@@ -1177,7 +1205,8 @@ struct lkv_device final : layersim::KvObserver {
         }
         LKV_CUDA(cudaGetLastError());
       }
-      if (timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attention kernel | merge kernel
+      // attention kernel | merge kernel (an event between them costs the PDL overlap: LKV_SPLIT_TIMING=0 drops it)
+      if (timing && split_timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));
       // merge (members without KV get zero rows: no chunks, L = 0)
       if (gather_on() && merge_version < 4) throw std::invalid_argument("fused gather needs merge v4/v5");
       if (merge_version == 2)
@@ -1188,8 +1217,7 @@ struct lkv_device final : layersim::KvObserver {
         decode_merge_v4_kernel<<<dim3(n, Hql), 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32,
                                                              gather_args(l));
       else
-        decode_merge_v5_kernel<<<dim3(n, Hql), 256, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32,
-                                                             gather_args(l));
+        launch_merge_v5(n, out, f32, gather_args(l));
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;
       dstats.kernel_launches += n_chunks > 0 ? 2 : 1;
@@ -1227,7 +1255,10 @@ struct lkv_device final : layersim::KvObserver {
       gather_flag_kernel<<<1, 1, 0, cs>>>(ga);
       LKV_CUDA(cudaGetLastError());
     }
-    if (timing) LKV_CUDA(cudaEventRecord(t_attn1[l], cs));
+    if (timing) {
+      if (!split_timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attn_ms = the pair
+      LKV_CUDA(cudaEventRecord(t_attn1[l], cs));
+    }
     LKV_CUDA(cudaEventRecord(attn_done[st], cs));
     attn_recorded[st] = 1;
     join_out(user);
