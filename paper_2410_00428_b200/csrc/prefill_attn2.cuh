@@ -85,7 +85,7 @@ template <int POLY>
 __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
-    float scale_log2) {
+    float scale_log2, int chunk_q) {
   using S = PrefillAttn2Smem;
   constexpr int NS = S::kStages;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -104,12 +104,21 @@ __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
 
   const int nq = (tokens + 127) / 128;
   const int npairs = (nq + 1) / 2;
-  const int pair = npairs - 1 - static_cast<int>(blockIdx.x);  // heaviest first
+  // 1D grid in dispatch order: query heads in chunks of `chunk_q` (whole GQA
+  // groups), and inside a chunk every head's heaviest pair first, heads
+  // fastest. Within a chunk that is longest-processing-time order, so the
+  // launch ends on the lightest pairs instead of a late heavy one; the chunk
+  // bounds the K/V the resident CTAs stream (chunk_q / G KV heads x T x
+  // 512 B) to what L2 holds, so those tiles are read from HBM about once.
+  const int chunk = static_cast<int>(blockIdx.x) / (chunk_q * npairs);
+  const int width = min(chunk_q, Hq - chunk * chunk_q);
+  const int within = static_cast<int>(blockIdx.x) - chunk * chunk_q * npairs;
+  const int pair = npairs - 1 - within / width;
   const int qa = 2 * pair, qb = 2 * pair + 1;
   const bool has_b = qb < nq;
   const int nt_a = qa + 1, nt_b = has_b ? qb + 1 : 0;
   const int nt = has_b ? nt_b : nt_a;  // KV tiles this CTA loads
-  const int hq = blockIdx.y, h = hq / G;
+  const int hq = chunk * chunk_q + within % width, h = hq / G;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
   if (threadIdx.x == 0) {
