@@ -10,20 +10,24 @@
 // kernel stays HBM-bound. P is split into bf16 hi + lo halves that fill the
 // padded columns, so the PV product is accurate to ~2^-16 relative.
 //
-// Roles, one persistent CTA per SM (192 threads):
-//   warp 0   producer: per unit writes Q into smem (K-major, no swizzle),
-//            per tile issues 2 x (128/bs) x 2 TMA tensor boxes {64 d, bs tok}
-//            of K and V from the paged slots straight into swizzle-128B
-//            tiles (the tensor map spans pool + arena frames, so resident
-//            and prefetched blocks are addressed alike through the snapshot);
-//   warp 1   MMA issuer (one thread) + TMEM owner: S^T(j+1) is issued before
-//            O^T(j) so the softmax of tile j overlaps the next QK^T;
+// Roles, one persistent CTA per SM (224 threads):
+//   warp 0   K producer: per unit writes Q into smem (K-major, no swizzle),
+//            per tile issues (128/bs) x 2 TMA tensor boxes {64 d, bs tok} of
+//            K from the paged slots straight into a swizzle-128B tile (the
+//            tensor map spans pool + arena frames, so resident and prefetched
+//            blocks are addressed alike through the snapshot);
+//   warp 6   V producer: the same for V, on its own ring. A K slot frees when
+//            its QK^T completes, a V slot when its PV does, so the softmax is
+//            on neither ring's refill cycle;
+//   warp 1   MMA issuer (one thread) + TMEM owner: S^T(j) is issued as soon
+//            as K(j) lands, PV(j-1) as soon as P(j-1) and V(j-1) are ready;
 //   warps 2-5 softmax/epilogue: thread = TMEM lane = token row of S^T and
-//            d row of O^T. Row max across the 128 tokens: warp butterfly +
-//            one named barrier; P^T goes to smem (MN-major, no swizzle) as
-//            the B operand of the PV MMA; each tile's O^T lands in a fresh
-//            TMEM buffer and is folded into registers with the online-
-//            softmax correction (no TMEM read-modify-write hazard).
+//            d row of O^T. Lazy running max (a bar.red.or vote; the exact
+//            per-head max only when a score exceeds it by 2^8); P^T goes to
+//            smem (MN-major, no swizzle) as the B operand of the PV MMA; each
+//            tile's O^T lands in a fresh TMEM buffer and is folded into
+//            registers with the online-softmax correction (no TMEM
+//            read-modify-write hazard).
 // Work unit = (chunk of blocks of one sequence, one KV head), exactly as the
 // CUDA-core kernel (decode_attn.cuh), and the partial (m, l, o) per query head
 // is merged by decode_merge_v3_kernel.
@@ -49,10 +53,10 @@ struct GqaTc {
   static constexpr int kOffRed = kOffP + 2 * 4096;     // [2][4][8] f32 tile maxima
   static constexpr int kOffLred = kOffRed + 256;       // [4][8] f32 row sums
   static constexpr int kOffBar = kOffLred + 128;       // mbarriers
-  static constexpr int kNumBars = 2 * NS + 14;
+  static constexpr int kNumBars = 4 * NS + 14;
   static constexpr int kOffTmem = kOffBar + kNumBars * 8;
   static constexpr int kSmem = kOffTmem + 16 + 1024;  // + alignment slack
-  static constexpr int kThreads = 192;
+  static constexpr int kThreads = 224;
   static_assert(kSmem <= 227 * 1024, "smem budget");
 };
 
@@ -82,7 +86,7 @@ __device__ __forceinline__ bool named_bar_or(int id, int n, bool v) {
 constexpr float kLazyMax = 8.f;
 
 template <int G, int BS, int NS>
-__global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
+__global__ void __launch_bounds__(224, 1) decode_gqa_tc_kernel(
     const __grid_constant__ CUtensorMap kvmap, int Hl, const int* __restrict__ snap,
     const AttnSeq* __restrict__ seqs, const AttnChunk* __restrict__ chunks, int n_units,
     const __nv_bfloat16* __restrict__ q, float* __restrict__ part_o, float* __restrict__ part_ml,
@@ -92,9 +96,11 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + C::kOffBar);
-  uint64_t* full = bars;             // [NS] TMA -> MMA
-  uint64_t* empty = bars + NS;       // [NS] MMA (PV done) -> TMA
-  uint64_t* s_full = bars + 2 * NS;  // [2] S^T in TMEM
+  uint64_t* kfull = bars;            // [NS] K half landed (TMA -> MMA)
+  uint64_t* kempty = bars + NS;      // [NS] QK^T done with the K half
+  uint64_t* vfull = bars + 2 * NS;   // [NS] V half landed
+  uint64_t* vempty = bars + 3 * NS;  // [NS] PV done with the V half
+  uint64_t* s_full = bars + 4 * NS;  // [2] S^T in TMEM
   uint64_t* s_empty = s_full + 2;    // [2] S^T read by softmax
   uint64_t* p_full = s_full + 4;     // [2] P^T in smem
   uint64_t* o_full = s_full + 6;     // [2] O^T tile in TMEM
@@ -108,8 +114,10 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
     for (int s = 0; s < NS; ++s) {
-      tc::bar_init(&full[s], 1);
-      tc::bar_init(&empty[s], 1);
+      tc::bar_init(&kfull[s], 1);
+      tc::bar_init(&kempty[s], 1);
+      tc::bar_init(&vfull[s], 1);
+      tc::bar_init(&vempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       tc::bar_init(&s_full[b], 1);
@@ -134,16 +142,22 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
   const int rows_per_frame = 2 * Hl * BS;
   pdl_launch_dependents();
 
-  if (warp == 0) {
-    // ------------------------------------------------------------ producer
+  if (warp == 0 || warp == 6) {
+    // ------------------------------------------------------------ producers
+    // warp 0 loads Q and the K half of each tile, warp 6 the V half. The two
+    // halves have their own rings: a K slot frees as soon as its QK^T is done,
+    // a V slot when its PV is, so the softmax sits on neither ring's cycle.
+    const bool kside = warp == 0;
+    uint64_t* ring_full = kside ? kfull : vfull;
+    uint64_t* ring_empty = kside ? kempty : vempty;
     int stage = 0, qb = 0;
     uint32_t ph = 0, qph = 0;
     for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
       const AttnChunk ck = chunks[u / Hl];
       const int h = u % Hl;
       const AttnSeq sd = seqs[ck.seq];
-      tc::bar_wait(&q_empty[qb], qph ^ 1u);
-      {
+      if (kside) {
+        tc::bar_wait(&q_empty[qb], qph ^ 1u);
         // Q rows g < G: chunk c = (g, d8) -> (d8 * 128 + g * 16) in the K-major core-matrix layout
         const __nv_bfloat16* qs = q + (static_cast<long long>(ck.seq) * Hl + h) * G * 128;
         uint8_t* qd = sm + C::kOffQ + qb * 4096;
@@ -155,10 +169,10 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
         tc::fence_async_smem();
         __syncwarp();
         if (lane == 0) tc::bar_arrive(&q_full[qb]);
-      }
-      if (++qb == 2) {
-        qb = 0;
-        qph ^= 1u;
+        if (++qb == 2) {
+          qb = 0;
+          qph ^= 1u;
+        }
       }
       const int ntile = (ck.nb + TB - 1) / TB;
       for (int t = 0; t < ntile; ++t) {
@@ -168,19 +182,16 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
           frame = snap[sd.blk_offset + ck.b0 + bi];
         }
         if (lane == 0) {
-          tc::bar_wait(&empty[stage], ph ^ 1u);
-          tc::bar_expect_tx(&full[stage], C::kStage);
+          tc::bar_wait(&ring_empty[stage], ph ^ 1u);
+          tc::bar_expect_tx(&ring_full[stage], C::kTile);
         }
         __syncwarp();
         if (lane < TB) {
           const int rk = frame * rows_per_frame + h * BS;
-          const int rv = rk + Hl * BS;
-          uint8_t* kt = sm + stage * C::kStage + lane * BS * 128;
+          const int row = kside ? rk : rk + Hl * BS;
+          uint8_t* dst = sm + stage * C::kStage + (kside ? 0 : C::kTile) + lane * BS * 128;
 #pragma unroll
-          for (int half = 0; half < 2; ++half) {
-            tc::tma_load_2d(kt + half * 16384, &kvmap, half * 64, rk, &full[stage]);
-            tc::tma_load_2d(kt + C::kTile + half * 16384, &kvmap, half * 64, rv, &full[stage]);
-          }
+          for (int half = 0; half < 2; ++half) tc::tma_load_2d(dst + half * 16384, &kvmap, half * 64, row, &ring_full[stage]);
         }
         __syncwarp();
         if (++stage == NS) {
@@ -200,49 +211,47 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
       unsigned j = 0;
       bool have_prev = false;
       int prev_stage = 0;
+      uint32_t prev_ph = 0;
       unsigned prev_j = 0;
-      auto issue_pv = [&](int st, unsigned jj) {
-        const int pb = jj & 1;
-        const uint32_t par = (jj >> 1) & 1u;
+      auto pv_ready = [&]() {
+        return tc::bar_test(&p_full[prev_j & 1], (prev_j >> 1) & 1u) && tc::bar_test(&vfull[prev_stage], prev_ph);
+      };
+      auto issue_pv = [&]() {
+        const int pb = prev_j & 1;
+        const uint32_t par = (prev_j >> 1) & 1u;
         tc::bar_wait(&p_full[pb], par);
         tc::bar_wait(&o_empty[pb], par ^ 1u);
+        tc::bar_wait(&vfull[prev_stage], prev_ph);
         tc::fence_after_sync();
-        const uint32_t vt = kv0 + st * C::kStage + C::kTile;
+        const uint32_t vt = kv0 + prev_stage * C::kStage + C::kTile;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
           tc::mma_bf16(tmem + 32 + pb * 16, tc::smem_desc(vt + kk * 2048, 16384, 1024, tc::kLayoutSw128),
                        tc::smem_desc(p0 + pb * 4096 + kk * 512, 256, 128, tc::kLayoutNone), idO, kk > 0);
         tc::mma_commit(&o_full[pb]);
-        tc::mma_commit(&empty[st]);
+        tc::mma_commit(&vempty[prev_stage]);
+        have_prev = false;
+      };
+      // PV(j-1) frees a V slot: issue it as soon as P(j-1) and V(j-1) are
+      // there, while waiting for whatever the next QK^T needs.
+      auto wait_or_pv = [&](uint64_t* bar, uint32_t parity) {
+        if (!have_prev) return;
+        while (!tc::bar_test(bar, parity)) {
+          if (pv_ready()) {
+            issue_pv();
+            return;
+          }
+        }
       };
       for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
         const AttnChunk ck = chunks[u / Hl];
         const int ntile = (ck.nb + TB - 1) / TB;
-        if (have_prev) {  // same for the previous unit's last PV while this unit's Q loads
-          while (!tc::bar_test(&q_full[qb], qph)) {
-            if (tc::bar_test(&p_full[prev_j & 1], (prev_j >> 1) & 1u)) {
-              issue_pv(prev_stage, prev_j);
-              have_prev = false;
-              break;
-            }
-          }
-        }
+        wait_or_pv(&q_full[qb], qph);
         tc::bar_wait(&q_full[qb], qph);
         for (int t = 0; t < ntile; ++t) {
           const int sb = j & 1;
-          // PV(j-1) frees its K/V stage for the producer: issue it as soon as
-          // P(j-1) is ready instead of behind the arrival of tile j, so a late
-          // tile never holds a finished stage (one more stage of loads in flight).
-          if (have_prev) {
-            while (!tc::bar_test(&full[stage], ph)) {
-              if (tc::bar_test(&p_full[prev_j & 1], (prev_j >> 1) & 1u)) {
-                issue_pv(prev_stage, prev_j);
-                have_prev = false;
-                break;
-              }
-            }
-          }
-          tc::bar_wait(&full[stage], ph);
+          wait_or_pv(&kfull[stage], ph);
+          tc::bar_wait(&kfull[stage], ph);
           tc::bar_wait(&s_empty[sb], ((j >> 1) & 1u) ^ 1u);
           tc::fence_after_sync();
           const uint32_t kt = kv0 + stage * C::kStage;
@@ -252,10 +261,12 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
                          tc::smem_desc(kt + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, tc::kLayoutSw128),
                          tc::smem_desc(q0 + qb * 4096 + kk * 256, 128, 2048, tc::kLayoutNone), idS, kk > 0);
           tc::mma_commit(&s_full[sb]);
+          tc::mma_commit(&kempty[stage]);
           if (t == ntile - 1) tc::mma_commit(&q_empty[qb]);
-          if (have_prev) issue_pv(prev_stage, prev_j);
+          if (have_prev) issue_pv();
           have_prev = true;
           prev_stage = stage;
+          prev_ph = ph;
           prev_j = j;
           ++j;
           if (++stage == NS) {
@@ -268,9 +279,9 @@ __global__ void __launch_bounds__(192, 1) decode_gqa_tc_kernel(
           qph ^= 1u;
         }
       }
-      if (have_prev) issue_pv(prev_stage, prev_j);
+      if (have_prev) issue_pv();
     }
-  } else {
+  } else if (warp <= 5) {
     // ------------------------------------------------------------ softmax / epilogue
     const int quad = warp & 3;
     const int r = quad * 32 + lane;  // TMEM lane: token row of S^T, d row of O^T
