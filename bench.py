@@ -482,6 +482,32 @@ def gqa_decode_row(torch, dev_t, hbm_peak, hq=32, hkv=8, tp_size=1, B=16, ctx=32
             "note": "peak is the measured copy (read+write) bandwidth; a read-only KV stream can exceed it"}
 
 
+def gqa_prefill_row(torch, dev_t, tf_peak, T=32768):
+    """a20 on config 3's prefill: Llama-3-8B GQA (Hq 32 / Hkv 8), a 32k-token
+    prompt, one layer's causal attention through lkv_prefill_attention."""
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+    model = ls.ModelSpec(1, 32, 8, 128, 4096, 8.03e9, 2)
+    kv = ls.KvManager(ls.BlockPools(64, 64, 16), model)
+    dev = Device(kv, model, 16, DeviceConfig(device=dev_t.index or 0, gpu_slots=64, host_slots=64, arena_slots=64,
+                                             max_requests=2, max_blocks=8, max_batch=1))
+    cs = dev.torch_stream("compute")
+    g = torch.Generator(device=dev_t).manual_seed(5)
+    q = (torch.rand((T, 32, 128), device=dev_t, generator=g) * 2 - 1).to(torch.bfloat16)
+    k = (torch.rand((T, 8, 128), device=dev_t, generator=g) * 2 - 1).to(torch.bfloat16)
+    v = (torch.rand((T, 8, 128), device=dev_t, generator=g) * 2 - 1).to(torch.bfloat16)
+    out = torch.empty_like(q)
+    attn = lambda: dev.prefill_attention(q, k, v, out, T, 1.0 / math.sqrt(128), DTYPE_BF16, stream=cs)  # noqa: E731
+    attn()
+    ms = min(ev_ms(torch, cs, attn) for _ in range(3))
+    flops = 4.0 * 128 * 32 * T * (T + 1) / 2
+    dev.close()
+    return {"kernel": "prefill_attn2_kernel (tcgen05, causal GQA)",
+            "shape": f"config 3, Llama-3-8B GQA Hq 32 / Hkv 8, {T} tokens, 1 layer", "ms": ms,
+            "tflops": flops / ms / 1e9, "peak_tflops": tf_peak, "frac": flops / ms / 1e9 / tf_peak,
+            "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)"}
+
+
 def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=3):
     """f3: config 2's decode iteration (7B, every layer CPU-resident) with the
     CPU slots' homes in pageable memory and only `pinned_frac` of them backed
@@ -557,16 +583,23 @@ def scatter_gather_row(torch, dev_t, hbm_peak, T=16384, L=4):
     dev.fill_kv(k, v, T, 0, 0, SEED, stream=cs)
     slot_bytes = dev.slot_bytes
     best_s = best_g = None
+    host_ms = []
     for _ in range(3):
         assert kv.allocate_prefill(0, T, L)  # every layer retained: scatter only
         torch.cuda.synchronize()
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
+        # keep the stream busy while the host enqueues, so the events time the
+        # device work and not the host's enqueue rate (reported beside it)
+        with torch.cuda.stream(cs):
+            torch.cuda._sleep(50_000_000)
         e0.record(cs)
+        t0 = time.perf_counter()
         for layer in range(L):
             dev.prefill_layer(0, layer, k, v, T, stream=cs)
         e1.record(cs)
         job = kv.plan_offload(0, ls.FULL)  # gather of all L x nblk GPU slots into staging (+ D2H on its stream)
         e2.record(cs)
+        host_ms.append((time.perf_counter() - t0) * 1e3)
         dev.synchronize()
         kv.complete_offload(job.job_id)
         kv.release(0)
@@ -580,6 +613,9 @@ def scatter_gather_row(torch, dev_t, hbm_peak, T=16384, L=4):
                         "frac": byts / (best_s / 1e3) / 1e9 / hbm_peak},
             "gather": {"kernel": "gather_slots_v2_kernel", "ms": best_g, "gbs": byts / (best_g / 1e3) / 1e9,
                        "frac": byts / (best_g / 1e3) / 1e9 / hbm_peak},
+            "host_enqueue_ms": min(host_ms),
+            "timing": "CUDA events on the compute stream, host enqueue hidden behind a sleep kernel "
+                      "(host_enqueue_ms = wall time of the enqueue calls)",
             "ncu": "profiles/r1w_scatter_gather_ncu.txt"}
 
 
@@ -823,6 +859,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_rows:  # §8 rows beside the headline (own devices, after this one is gone)
             rows = prefill_rows(torch, dev_t, link, tensor_peak())
+            rows["a20_prefill_attention_config3_32k"] = gqa_prefill_row(torch, dev_t, tensor_peak())
             rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak, B=64, label="config 3, 8B GQA")
             rows["a18_gqa_decode_70b_tp8_shard"] = gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8, tp_size=8,
                                                                   B=64, ctx=32768, label="70B GQA TP8 rank 0")
