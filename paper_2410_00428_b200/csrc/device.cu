@@ -1412,27 +1412,28 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   // LKV_PREFILL_KERNEL=1: the one-tile kernel (row halves); default with fp16
   // P: two query tiles per CTA, one softmax warpgroup each (prefill_attn2.cuh).
   const char* ek = std::getenv("LKV_PREFILL_KERNEL");
-  const bool two_tile = !(ek && std::atoi(ek) == 1);
+  const int kver = ek ? std::atoi(ek) : 2;
+  const bool two_tile = kver != 1;
+  const int nq_all = static_cast<int>((tokens + 127) / 128);
+  // KV heads per dispatch chunk: as many as keep their K+V (T x 512 B per
+  // KV head, bf16 K + fp16 V) within 16 MB (LKV_PREFILL_L2_MB; measured
+  // best of 0 / 16 / 48 / 96 / all, profiles/r1ab_prefill_order.jsonl).
+  // LKV_PREFILL_L2_MB=0: one query head per chunk (pairs fastest).
+  static const long long l2_budget = [] {
+    const char* e = std::getenv("LKV_PREFILL_L2_MB");
+    return (e ? std::max(0ll, std::atoll(e)) : 16ll) << 20;
+  }();
+  const long long kv_per_head = static_cast<long long>(tokens) * 512;
+  const int chunk_kv = static_cast<int>(std::clamp<long long>(l2_budget / std::max(kv_per_head, 1ll), 1, d->Hl));
+  const int chunk_q = l2_budget == 0 ? 1 : chunk_kv * d->G;
+  const long long npairs_all = (nq_all + 1) / 2;
   if (pf16 && two_tile) {
     // LKV_PREFILL_POLY = 0 / 25 / 50: share of exponentials computed on the FMA pipe
     const char* epo = std::getenv("LKV_PREFILL_POLY");
     const int poly = epo ? std::atoi(epo) : 0;
     auto fn2 = poly >= 50 ? prefill_attn2_kernel<2> : poly >= 25 ? prefill_attn2_kernel<1> : prefill_attn2_kernel<0>;
     d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
-    const int nq = static_cast<int>((tokens + 127) / 128);
-    const long long npairs = (nq + 1) / 2;
-    // KV heads per dispatch chunk: as many as keep their K+V (T x 512 B per
-    // KV head, bf16 K + fp16 V) within 16 MB (LKV_PREFILL_L2_MB; measured
-    // best of 0 / 16 / 48 / 96 / all, profiles/r1ab_prefill_order.jsonl).
-    // LKV_PREFILL_L2_MB=0: one query head per chunk (pairs fastest).
-    static const long long l2_budget = [] {
-      const char* e = std::getenv("LKV_PREFILL_L2_MB");
-      return (e ? std::max(0ll, std::atoll(e)) : 16ll) << 20;
-    }();
-    const long long kv_per_head = static_cast<long long>(tokens) * 512;
-    const int chunk_kv = static_cast<int>(std::clamp<long long>(l2_budget / std::max(kv_per_head, 1ll), 1, d->Hl));
-    const int chunk_q = l2_budget == 0 ? 1 : chunk_kv * d->G;
-    fn2<<<static_cast<unsigned>(npairs * d->Hql), 320, PrefillAttn2Smem::kBytes, s>>>(
+    fn2<<<static_cast<unsigned>(npairs_all * d->Hql), 320, PrefillAttn2Smem::kBytes, s>>>(
         qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
         scale * 1.4426950408889634f, chunk_q);
     LKV_CUDA(cudaGetLastError());
