@@ -751,7 +751,7 @@ def main():
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    attn_ms = h2d_ms = merge_ms = 0.0
+    attn_ms = h2d_ms = merge_ms = kern_ms = 0.0
     launches = attn_launches = 0
     h2d_alg = h2d_phys = kv_read = 0
     with ClockSampler(local) as clk:
@@ -761,6 +761,7 @@ def main():
             st = dev.decode_stats()
             attn_ms += st.attn_ms
             merge_ms += st.merge_ms
+            kern_ms += st.kernel_ms
             h2d_ms += st.h2d_ms
             launches += st.kernel_launches + (L if fused else 0)  # + the per-layer gather_wait_kernel
             attn_launches += st.attn_launches
@@ -833,7 +834,13 @@ def main():
                          "timed_as": "one CUDA-event interval per layer around the attention kernel and its split "
                                      "merge (launched as a programmatic dependent, no event between them)",
                          "peak_kind": peak_kind,
-                         "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms},
+                         "bytes_per_launch": per_launch_bytes, "avg_launch_ms": avg_launch_ms,
+                         "attention_kernel_alone": {
+                             "avg_ms": kern_ms / max(attn_launches, 1),
+                             "frac": per_launch_bytes / (kern_ms / max(attn_launches, 1) / 1000) / 1e9 / hbm_peak
+                             if kern_ms > 0 else None,
+                             "timer": "%globaltimer, first CTA start to last warp end of each attention kernel "
+                                      "(excludes launch latency and the merge; diagnostic beside the event time)"}},
             "host_link": {"prefetch_gbs_per_gpu": h2d_alg / world / (h2d_ms / 1000) / 1e9 if h2d_ms else None,
                           "prefetch_algorithmic_bytes_per_step": h2d_alg // args.steps * world,
                           "prefetch_physical_bytes_per_step": h2d_phys // args.steps * world,

@@ -366,6 +366,8 @@ typedef struct lkv_decode_stats {
   double iteration_ms;           /* decode_begin -> decode_end on the device */
   double h2d_span_ms;            /* first prefetch copy start -> last prefetch copy end */
   double merge_ms;               /* split-merge time when LKV_SPLIT_TIMING=1, else 0 (inside attn_ms) */
+  double kernel_ms;              /* attention kernels alone: first CTA start -> last warp end on %globaltimer,
+                                    summed over layers (no launch latency, no merge) */
 } lkv_decode_stats;
 LKV_API int lkv_device_set_timing(lkv_device* dev, int32_t on);
 LKV_API int lkv_decode_last_stats(const lkv_device* dev, lkv_decode_stats* out);

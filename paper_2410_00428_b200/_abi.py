@@ -120,7 +120,7 @@ class DecodeStats(C.Structure):
     _fields_ = [("h2d_bytes_physical", i64), ("h2d_bytes_algorithmic", i64), ("h2d_copies", i64),
                 ("kv_bytes_read", i64), ("attn_launches", i64), ("kernel_launches", i64), ("attn_ms", f64),
                 ("h2d_ms", f64),
-                ("iteration_ms", f64), ("h2d_span_ms", f64), ("merge_ms", f64)]
+                ("iteration_ms", f64), ("h2d_span_ms", f64), ("merge_ms", f64), ("kernel_ms", f64)]
 
 
 class OffloadStats(C.Structure):

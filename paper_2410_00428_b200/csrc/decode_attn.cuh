@@ -52,6 +52,23 @@ __device__ __forceinline__ void pdl_launch_dependents() {
 }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Kernel span stamps (timing mode): the first CTA's start and the last
+// warp's end on %globaltimer, so the attention kernel's own duration can be
+// told apart from launch latency in the event-timed interval.
+__device__ __forceinline__ unsigned long long global_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// st[0] keeps ~start (atomicMax of the complement = earliest start), so a
+// zeroed pair is the initial state.
+__device__ __forceinline__ void stamp_begin(unsigned long long* st) {
+  if (st && threadIdx.x == 0) atomicMax(st, ~global_ns());
+}
+__device__ __forceinline__ void stamp_end(unsigned long long* st) {
+  if (st && (threadIdx.x & 31) == 0) atomicMax(st + 1, global_ns());
+}
+
 __device__ __forceinline__ unsigned smem_addr(const void* p) {
   return static_cast<unsigned>(__cvta_generic_to_shared(p));
 }
@@ -187,7 +204,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_attn_v2_kernel(
     const char* __restrict__ base, long long slot_bytes, int Hl, const int* __restrict__ snap,
     const AttnSeq* __restrict__ seqs, const AttnChunk* __restrict__ chunks, int n_units,
     const __nv_bfloat16* __restrict__ q, float* __restrict__ part_o, float* __restrict__ part_ml,
-    float scale_log2) {
+    float scale_log2, unsigned long long* stamps) {
   using C = AttnV2<G, BS, W, S>;
   constexpr int D = kHeadDim;
   constexpr int SUB = C::kSubPerBlock;
@@ -204,6 +221,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_attn_v2_kernel(
   __syncwarp();
 
   pdl_launch_dependents();
+  stamp_begin(stamps);
   const int gw = blockIdx.x * W + warp;
   const int NW = gridDim.x * W;
   const long long tile_bytes = static_cast<long long>(BS) * D * 2;
@@ -362,6 +380,7 @@ __global__ void __launch_bounds__(W * 32, 1) decode_attn_v2_kernel(
       }
     }
   }
+  stamp_end(stamps);
 }
 
 // One warp per (member, query head); 4 warps per CTA.

@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(224, 1) decode_gqa_tc_kernel(
     const __grid_constant__ CUtensorMap kvmap, int Hl, const int* __restrict__ snap,
     const AttnSeq* __restrict__ seqs, const AttnChunk* __restrict__ chunks, int n_units,
     const __nv_bfloat16* __restrict__ q, float* __restrict__ part_o, float* __restrict__ part_ml,
-    float scale_log2) {
+    float scale_log2, unsigned long long* stamps) {
   using C = GqaTc<G, BS, NS>;
   constexpr int TB = C::kTB;
   extern __shared__ uint8_t smem_raw[];
@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(224, 1) decode_gqa_tc_kernel(
   const uint32_t tmem = *tmem_slot;
   const int rows_per_frame = 2 * Hl * BS;
   pdl_launch_dependents();
+  stamp_begin(stamps);
 
   if (warp == 0 || warp == 6) {
     // ------------------------------------------------------------ producers
@@ -405,6 +406,7 @@ __global__ void __launch_bounds__(224, 1) decode_gqa_tc_kernel(
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) tc::tmem_free<64>(tmem);
+  if (warp == 0) stamp_end(stamps);
 }
 
 }  // namespace lkv

@@ -146,6 +146,8 @@ struct lkv_device final : layersim::KvObserver {
   }
   int* d_table = nullptr;      // [max_requests][L][max_blocks]
   int* d_snap = nullptr;       // [L][arena_slots]
+  unsigned long long* d_stamps = nullptr;  // timing: [L][2] attention kernel span (%globaltimer min start, max end)
+  unsigned long long* layer_stamps(int l) { return timing && d_stamps ? d_stamps + 2 * l : nullptr; }
   SeqDesc* d_seqs = nullptr;   // [max_batch]
   char* d_staging = nullptr;   // staging_chunks x seg bytes
   unsigned* d_slotlist = nullptr;  // staging_chunks x seg_slots GPU slot ids
@@ -394,6 +396,7 @@ struct lkv_device final : layersim::KvObserver {
     cudaFree(d_xlat);
     cudaFree(d_table);
     cudaFree(d_snap);
+    cudaFree(d_stamps);
     cudaFree(d_seqs);
     cudaFree(d_staging);
     cudaFree(d_slotlist);
@@ -908,6 +911,10 @@ struct lkv_device final : layersim::KvObserver {
     LKV_CUDA(cudaEventRecord(ev, d2h));
     LKV_CUDA(cudaStreamWaitEvent(h2d, ev, 0));
     cudaEventDestroy(ev);
+    if (timing) {
+      if (!d_stamps) LKV_CUDA(cudaMalloc(&d_stamps, static_cast<std::size_t>(std::max(L, 1)) * 16));
+      LKV_CUDA(cudaMemsetAsync(d_stamps, 0, static_cast<std::size_t>(std::max(L, 1)) * 16, cs));
+    }
     in_iteration = true;
     for (int l = 0; l < std::min(cfg.pipeline_depth, L); ++l) issue_fetch(l);
   }
@@ -992,7 +999,7 @@ struct lkv_device final : layersim::KvObserver {
     const int grid = std::max(1, std::min(sms, units));
     fn<<<grid, K::kThreads, K::kSmem, cs>>>(kvmap, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
                                             d_aseqs, d_chunks, units, static_cast<const __nv_bfloat16*>(q),
-                                            d_part_o, d_part_ml, sl2);
+                                            d_part_o, d_part_ml, sl2, layer_stamps(l));
   }
 
   template <int GG>
@@ -1011,7 +1018,7 @@ struct lkv_device final : layersim::KvObserver {
     const int grid = std::max(1, std::min(sms, (units + W - 1) / W));
     fn<<<grid, K::kThreads, K::kSmem, cs>>>(dbuf, sb, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
                                             d_aseqs, d_chunks, units, static_cast<const __nv_bfloat16*>(q),
-                                            d_part_o, d_part_ml, sl2);
+                                            d_part_o, d_part_ml, sl2, layer_stamps(l));
   }
 
   template <int GG, int BB>
@@ -1604,6 +1611,16 @@ int lkv_decode_last_stats(const lkv_device* dc, lkv_decode_stats* out) {
     cudaGetLastError();
     out->attn_ms = attn;
     out->merge_ms = merge;
+    if (d->d_stamps) {  // attention kernels' own span (%globaltimer), beside the event-timed interval
+      std::vector<unsigned long long> st(static_cast<std::size_t>(d->L) * 2);
+      LKV_CUDA(cudaMemcpy(st.data(), d->d_stamps, st.size() * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+      double k = 0.0;
+      for (int l = 0; l < d->L; ++l) {
+        const unsigned long long t0 = ~st[2 * l], t1 = st[2 * l + 1];
+        if (st[2 * l] != 0ull && t1 > t0) k += static_cast<double>(t1 - t0) * 1e-6;
+      }
+      out->kernel_ms = k;
+    }
     if (d->h2d_started && cudaEventElapsedTime(&ms, d->t_h2d0, d->t_h2d1) == cudaSuccess)
       out->h2d_span_ms = ms;
     cudaGetLastError();
