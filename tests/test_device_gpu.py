@@ -184,6 +184,8 @@ def test_decode_stats_accounting():
     assert st.h2d_bytes_algorithmic == fetch  # == reference plan_decode_fetch bytes
     assert st.kv_bytes_read == 100 * kvb * 4
     assert st.attn_launches == 4 and st.attn_ms > 0 and st.iteration_ms > 0
+    # the kernels' own %globaltimer span sits inside the event-timed attention intervals
+    assert 0 < st.kernel_ms <= st.attn_ms + 0.05
 
 
 def test_capacity_error_is_loud():
