@@ -244,7 +244,8 @@ def reference_arm(args):
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload_config(args),
             "impl": "reference",
             "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
-            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "host": host_info()}
     print(json.dumps(line), flush=True)
 
 
@@ -296,6 +297,22 @@ def simulated_ttft(ctx):
 
 
 # ------------------------------------------------------------------ §8 rows beside the headline
+def host_info():
+    """The box's host side, stated beside the CPU numbers."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    info["cpu"] = line.split(":", 1)[1].strip()
+                    break
+        with open("/proc/meminfo") as f:
+            info["mem_total_gb"] = round(int(f.readline().split()[1]) / 1e6, 1)
+    except (OSError, ValueError, IndexError):
+        pass
+    return info
+
+
 def ev_ms(torch, stream, fn, iters=1):
     """CUDA-event time of fn() on `stream` (synchronised on both sides)."""
     torch.cuda.synchronize()
@@ -858,6 +875,7 @@ def main():
             "rows": None,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "host": host_info(),
         }
     # pinned tensors used on the device's streams must go before the streams do
     del q_host, out_host, q, out, k, v, gathered
