@@ -14,5 +14,5 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:deco
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:prefill_attn2 -c 1 \
   -o $O/prefill_attn2_$TAG -f python scripts/prefill_micro.py --tokens 8192 --iters 1 > $O/ncu_pf_$TAG.log 2>&1; echo "ncu prefill rc=$?"
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:decode_gqa_tc -c 1 \
-  -o $O/decode_gqa_tc_$TAG -f python scripts/attn_micro.py --group 8 --ctx 16384 --batch 8 --layers 1 --iters 1 > $O/ncu_gqa_$TAG.log 2>&1; echo "ncu gqa rc=$?"
+  -o $O/decode_gqa_tc_$TAG -f python scripts/attn_micro.py --group 8 --hkv 1 --ctx 32768 --batch 64 --layers 1 --iters 1 > $O/ncu_gqa_$TAG.log 2>&1; echo "ncu gqa rc=$?"
 ls -la $O
