@@ -1440,9 +1440,18 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
     const int poly = epo ? std::atoi(epo) : 0;
     auto fn2 = poly >= 50 ? prefill_attn2_kernel<2> : poly >= 25 ? prefill_attn2_kernel<1> : prefill_attn2_kernel<0>;
     d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
-    fn2<<<static_cast<unsigned>(npairs_all * d->Hql), 320, PrefillAttn2Smem::kBytes, s>>>(
-        qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
-        scale * 1.4426950408889634f, chunk_q);
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));
+    lc.blockDim = dim3(320);
+    lc.dynamicSmemBytes = PrefillAttn2Smem::kBytes;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = at;
+    lc.numAttrs = d->pdl ? 1 : 0;  // dependent of bf16_to_f16_kernel (LKV_PDL=0: plain launch)
+    LKV_CUDA(cudaLaunchKernelEx(&lc, fn2, qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0,
+                                static_cast<int>(tokens), d->Hql, d->G, scale * 1.4426950408889634f, chunk_q));
     LKV_CUDA(cudaGetLastError());
     LKV_CUDA(cudaEventRecord(d->vh_free, s));
     d->vh_used = true;

@@ -485,7 +485,11 @@ __global__ void fill_kv_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat16* __r
 
 // bf16 -> fp16, 8 values per thread step (the PF16 prefill attention's V
 // copy). Exact for |x| in fp16's normal range [2^-14, 65504].
+// The prefill attention is launched as its programmatic dependent: it loads
+// Q and K and starts QK^T while this runs, and waits (griddepcontrol.wait)
+// only before its first V load.
 __global__ void bf16_to_f16_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, long long n8) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
     const uint4 a = __ldcs(src + i);
     const uint32_t w[4] = {a.x, a.y, a.z, a.w};

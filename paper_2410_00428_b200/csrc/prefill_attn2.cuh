@@ -164,6 +164,9 @@ __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
         tc::tma_load_3d(kt, &kmap, 0, h, j * 128, &k_full[st]);
         tc::tma_load_3d(kt + 16384, &kmap, 64, h, j * 128, &k_full[st]);
         tc::bar_wait(&v_empty[st], ph);
+        // V is the fp16 copy the preceding kernel writes (PDL primary): wait
+        // for it once, before the first V load (no-op without PDL)
+        if (j == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
         tc::bar_expect_tx(&v_full[st], 32768);
         uint8_t* vt = sm + S::kV + st * 32768;
         tc::tma_load_3d(vt, &vmap, 0, h, j * 128, &v_full[st]);
