@@ -61,6 +61,7 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-seconds", type=float, default=12.0)
     p.add_argument("--no-rows", action="store_true", help="skip the tensor-core / overlap rows beside the headline")
+    p.add_argument("--rows", default="all", help="comma-separated subset of the rows beside the headline")
     p.add_argument("--allgather", default="fused", choices=["fused", "nccl"],
                    help="N>1 exchange of per-head outputs: fused into the merge kernel over NVLink peer memory "
                         "(product) or a separate NCCL all-gather (baseline)")
@@ -499,6 +500,89 @@ def gqa_decode_row(torch, dev_t, hbm_peak, hq=32, hkv=8, tp_size=1, B=16, ctx=32
             "note": "peak is the measured copy (read+write) bandwidth; a read-only KV stream can exceed it"}
 
 
+def config3_offload_row(torch, dev_t, link, hbm_peak, B=24, ctx=32768, steps=2):
+    """Config 3 with its layers offloaded and re-fetched per layer (engine.cpp:405-453):
+    Llama-3-8B GQA (Hq 32 / Hkv 8, G = 4), 32k prompts. Under the reference's schedule for this
+    config every layer of every request is CPU-resident (tests/golden/engine.json cfg3_b64: 274.9 GB
+    of D2H = 64 x 32 layers x 32k x 4 KiB), so each decode iteration re-fetches everything. 64 x 4.3 GB
+    exceeds the GPU box's host RAM (206 GB); the batch here is the largest whose CPU-resident KV
+    (pinned) fits beside the process: 24 x 4.3 GB = 103 GB (reference schedule for that batch:
+    cfg3_b24, also fully offloaded). Setup: the real prefill offload path per layer (generator K/V,
+    pack, D2H); step: decode_begin, then per layer the H2D prefetch into the arena (layer-ahead) and
+    the tcgen05 GQA decode tile over it."""
+    from paper_2410_00428_b200 import layersim as ls
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+    model = ls.llama3_8b_gqa()
+    L, bs, d = model.n_layers, 16, model.d_head
+    nblk = ctx // bs
+    slots = B * nblk * L
+    g = 2221882 * B // 64
+    kv = ls.KvManager(ls.BlockPools(g, g * 8, bs), model)
+    dev = Device(kv, model, bs, DeviceConfig(device=dev_t.index or 0, gpu_slots=64, host_slots=slots + 64,
+                                             arena_slots=B * nblk + 16, max_requests=B + 1, max_blocks=nblk + 4,
+                                             max_batch=B, staging_chunks=16, chunk_bytes=16 << 20))
+    cs = dev.torch_stream("compute")
+    hl, hq = dev.kv_heads_local, dev.q_heads_local
+    k = torch.empty((ctx, hl, d), dtype=torch.bfloat16, device=dev_t)
+    v = torch.empty_like(k)
+    ids = list(range(B))
+    dev.offload_stats(reset=True)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for rid in ids:
+        assert kv.allocate_prefill(rid, ctx, 0)
+        for layer in range(L):
+            dev.fill_kv(k, v, ctx, 0, layer, SEED, stream=cs)
+            dev.prefill_layer(rid, layer, k, v, ctx, stream=cs)
+    dev.synchronize()
+    t_off = time.perf_counter() - t0
+    ost = dev.offload_stats(reset=True)
+    q = torch.randn((B, hq, d), dtype=torch.bfloat16, device=dev_t)
+    out = torch.empty_like(q)
+    dev.set_timing(True)
+    times, stats = [], []
+    for it in range(steps + 1):
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(cs)
+        dev.decode_begin(ids)
+        for layer in range(L):
+            dev.decode_layer(layer, q, out, 1 / math.sqrt(d), DTYPE_BF16, stream=cs)
+        dev.decode_end()
+        e1.record(cs)
+        dev.synchronize()
+        st = dev.decode_stats()
+        if it >= 1:
+            times.append(e0.elapsed_time(e1))
+            stats.append(st)
+    bad = dev.verify_request(B - 1, ctx, SEED)
+    dev.close()
+    del k, v, q, out
+    step_ms = statistics.mean(times)
+    h2d = statistics.mean(s.h2d_bytes_algorithmic for s in stats)
+    h2d_busy_ms = statistics.mean(s.h2d_ms for s in stats)
+    pair_ms = statistics.mean((s.attn_ms + s.merge_ms) / max(1, s.attn_launches) for s in stats)
+    kern_ms = statistics.mean(s.kernel_ms / max(1, s.attn_launches) for s in stats)
+    per_launch = B * ctx * ls.kv_bytes_per_token_layer(model) + 2 * B * hq * d * 2
+    return {"workload": (f"config 3 decode iteration, Llama-3-8B GQA (Hq 32 / Hkv 8), {B} x {ctx} tokens, all {L} "
+                         f"layers CPU-resident (reference schedule cfg3_b{B}/cfg3_b64), pinned KV "
+                         f"{slots * dev.slot_bytes / 1e9:.0f} GB"),
+            "batch_note": "64 x 4.3 GB of CPU-resident KV exceeds the box's host RAM; 24 is the largest batch that fits",
+            "step_ms": step_ms, "steps": steps,
+            "prefetch_gbs": h2d / (step_ms / 1e3) / 1e9, "link_h2d_peak_gbs": link["h2d"],
+            "prefetch_frac_of_link": h2d / (step_ms / 1e3) / 1e9 / link["h2d"],
+            "prefetch_gbs_while_busy": h2d / (h2d_busy_ms / 1e3) / 1e9 if h2d_busy_ms else None,
+            "prefetch_bytes_per_step": h2d,
+            "attention": {"kernel": "decode_gqa_tc_kernel (tcgen05, G=4) + decode_merge_v5_kernel",
+                          "ms_per_layer": pair_ms, "gbs": per_launch / (pair_ms / 1e3) / 1e9,
+                          "frac": per_launch / (pair_ms / 1e3) / 1e9 / hbm_peak,
+                          "kernel_alone_frac": per_launch / (kern_ms / 1e3) / 1e9 / hbm_peak if kern_ms else None,
+                          "hidden_under_prefetch": L * pair_ms < step_ms},
+            "setup_offload_gbs": ost.d2h_bytes_algorithmic / t_off / 1e9, "setup_offload_bytes": ost.d2h_bytes_algorithmic,
+            "kv_verified_mismatches": bad,
+            "timing": "CUDA events on the compute stream around decode_begin..decode_end, mean of the timed steps"}
+
+
 def gqa_prefill_row(torch, dev_t, tf_peak, T=32768):
     """a20 on config 3's prefill: Llama-3-8B GQA (Hq 32 / Hkv 8), a 32k-token
     prompt, one layer's causal attention through lkv_prefill_attention."""
@@ -883,14 +967,31 @@ def main():
     dev.close()
     if rank == 0:
         if world == 1 and not args.no_rows:  # §8 rows beside the headline (own devices, after this one is gone)
-            rows = prefill_rows(torch, dev_t, link, tensor_peak())
-            rows["a20_prefill_attention_config3_32k"] = gqa_prefill_row(torch, dev_t, tensor_peak())
-            rows["a18_gqa_decode"] = gqa_decode_row(torch, dev_t, hbm_peak, B=64, label="config 3, 8B GQA")
-            rows["a18_gqa_decode_70b_tp8_shard"] = gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8, tp_size=8,
-                                                                  B=64, ctx=32768, label="70B GQA TP8 rank 0")
-            rows["a6_a8_scatter_gather"] = scatter_gather_row(torch, dev_t, hbm_peak)
-            rows["f1_measured_serving"] = serving_row(link, tensor_peak(), hbm_peak)
-            rows["f3_tiered_host_decode"] = tiered_host_row(torch, dev_t, link)
+            tf = tensor_peak()
+            table = {
+                "prefill": lambda: prefill_rows(torch, dev_t, link, tf),
+                "a20_prefill_attention_config3_32k": lambda: gqa_prefill_row(torch, dev_t, tf),
+                "a18_gqa_decode": lambda: gqa_decode_row(torch, dev_t, hbm_peak, B=64, label="config 3, 8B GQA"),
+                "a18_gqa_decode_70b_tp8_shard": lambda: gqa_decode_row(torch, dev_t, hbm_peak, hq=64, hkv=8,
+                                                                       tp_size=8, B=64, ctx=32768,
+                                                                       label="70B GQA TP8 rank 0"),
+                "config3_offload": lambda: config3_offload_row(torch, dev_t, link, hbm_peak),
+                "a6_a8_scatter_gather": lambda: scatter_gather_row(torch, dev_t, hbm_peak),
+                "f1_measured_serving": lambda: serving_row(link, tf, hbm_peak),
+                "f3_tiered_host_decode": lambda: tiered_host_row(torch, dev_t, link),
+            }
+            want = None if args.rows == "all" else set(args.rows.split(","))
+            rows = {}
+            for name, fn in table.items():
+                if want is not None and name not in want:
+                    continue
+                t0 = time.perf_counter()
+                r = fn()
+                if name == "prefill":
+                    rows.update(r)
+                else:
+                    rows[name] = r
+                    r["row_wall_s"] = time.perf_counter() - t0
             line["rows"] = rows
         print(json.dumps(line), flush=True)
     if world > 1:

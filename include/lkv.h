@@ -449,6 +449,8 @@ typedef struct lkv_serve_config { /* reference EngineConfig, engine.hpp:32-50 */
   int64_t ffn;               /* MLP width of the dense GEMMs; 0 = derived from n_param */
   int64_t host_slots;        /* pinned host frames; 0 = cpu_blocks */
   uint64_t kv_seed;          /* generator seed of the synthetic K/V */
+  int32_t tp_rank;           /* KV-head shard the device executes (tp_size = hw.n_gpus) */
+  int32_t pad_;
 } lkv_serve_config;
 
 typedef struct lkv_serve_summary { /* MetricsReport (metrics.hpp) + transfer totals + device stats */

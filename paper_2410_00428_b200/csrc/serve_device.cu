@@ -82,6 +82,7 @@ struct DeviceOptions {
   std::int64_t ffn = 0;
   std::int64_t host_slots = 0;
   std::uint64_t kv_seed = 0x4C61796572ull;
+  int tp_rank = 0;
 };
 
 struct TraceShape {
@@ -99,8 +100,8 @@ class DeviceExecutor final : public lkv::Executor {
     lkv_model_spec ms{m.n_layers, m.n_heads, m.n_kv_heads, m.d_head, m.hidden, m.n_param, m.f_precision, 0};
     lkv_device_config dc{};
     dc.device = o.device;
-    dc.tp_rank = 0;
-    dc.tp_size = 1;
+    dc.tp_rank = o.tp_rank;  // one KV-head shard of hw.n_gpus (the slot ids are the same on every rank)
+    dc.tp_size = cfg.hw.n_gpus;
     dc.pipeline_depth = o.depth;
     // Frames: the LIFO pools keep the highest slot id at the peak concurrent
     // use, which never exceeds every request of the trace held at once.
@@ -419,6 +420,11 @@ int lkv_serve_run(const lkv_serve_config* c, int32_t n, const int64_t* ids, cons
     o.ffn = c->ffn;
     o.host_slots = c->host_slots;
     o.kv_seed = c->kv_seed;
+    o.tp_rank = c->tp_rank;
+    if (c->tp_rank < 0 || c->tp_rank >= std::max(1, c->hw.n_gpus)) {
+      lkv::set_error("invalid argument: lkv_serve_run tp_rank outside [0, hw.n_gpus)");
+      return LKV_ERR_INVALID;
+    }
     TraceShape shape;
     shape.n = n;
     for (const auto& r : trace.requests) {

@@ -22,6 +22,27 @@ import oracle  # noqa: E402
 from paper_2410_00428_b200 import layersim as ls  # noqa: E402
 from tests import _drivers as drv  # noqa: E402
 
+B200_HW = dict(flops=1.3814e15, hbm_bandwidth=6.5367e12, pcie_bandwidth=5.5e10, nvlink=True, n_gpus=1,
+               gpu_mem=180e9, kv_reserve_fraction=0.9)  # SURVEY App. B's B200-like spec for configs 3-5
+
+
+def _pools(model, bs, hw=None, n_gpus=1):
+    """reference pool_size_from_hardware (kv_manager.cpp:10-32) at block size `bs`, restated in
+    Python so the scenario table is importable without a library (fixed numbers, pinned by
+    tests/test_kv_manager.py against both libraries)."""
+    import math
+    m = getattr(ls, model)()
+    h = dict(B200_HW if hw == "b200" else dict(gpu_mem=48e9, kv_reserve_fraction=0.9))
+    weight = m.n_param * m.f_precision
+    act = 2.0 * 16384 * m.hidden * m.f_precision * 4.0
+    kvb = (h["gpu_mem"] * n_gpus - weight - act) * h["kv_reserve_fraction"]
+    g = int(math.floor(kvb / (bs * 2 * m.n_kv_heads * m.d_head * m.f_precision)))
+    return g, int(math.floor(g * 8.0))
+
+
+CFG5_POOLS_7B = {bs: _pools("llama2_7b", bs) for bs in (16, 32, 64)}
+CFG5_POOLS_70B = {bs: _pools("llama31_70b_gqa", bs, "b200", 8) for bs in (16, 32, 64)}
+
 ENGINE_SCENARIOS = {
     # BASELINE.md §2 config 1: one request {0, 1024, 65}, pools {200000, 800000}
     **{f"cfg1_x{x}": dict(model="llama2_7b", pools=(200000, 800000), layerkv=True, force=x,
@@ -47,6 +68,33 @@ ENGINE_SCENARIOS = {
     # 70B GQA, TP8 over NVLink, half retained (config 4 shape, 4k + 64)
     "cfg4_tp8": dict(model="llama31_70b_gqa", tp=8, nvlink=True, pools=(2000000, 16000000), layerkv=True, force=40,
                      trace=("single", 4096, 65)),
+    # the same on the B200-like spec at TP 1/2/4/8: the cost model's prefill/decode times scale with TP
+    # (cost_model.cpp:39-44, 73-79; TTFT 0.4189/0.2094/0.1047/0.05236 s), the job bytes do not
+    **{f"cfg4_b200_tp{tp}": dict(model="llama31_70b_gqa", hw="b200", tp=tp, nvlink=True, pools=(2000000, 16000000),
+                                 layerkv=True, force=40, trace=("single", 4096, 65)) for tp in (1, 2, 4, 8)},
+    # config 2 at the two remaining BASELINE.md contexts
+    **{f"cfg2_{pol}_{ctx}": dict(model="llama2_7b", pools=(113043, 904344), layerkv=(pol == "layerkv"),
+                                 force=-1, seed=1, trace=("fixed", 100, ctx, 512, 1.0, 1))
+       for ctx in (512, 8192) for pol in ("baseline", "layerkv")},
+    # config 3: Llama-3-8B GQA (no preset: override), B200-like HardwareSpec, pools from
+    # pool_size_from_hardware(180 GB, max_input_tokens 32768); 64 x {0.0, 32768, 65}; max_batch_tokens
+    # admits the whole batch (p50/p99 TTFT 12.39/24.79 s, 2017 D2H / 131072 H2D jobs)
+    "cfg3_b64": dict(model="llama3_8b_gqa", hw="b200", pools=(2221882, 17775056), layerkv=True, force=-1,
+                     max_batch_tokens=64 * (32768 + 65), trace=("batch", 64, 32768, 65)),
+    # the same at the batches device runs use (host RAM holds 24 x 4.3 GB CPU-resident), with the GPU pool
+    # scaled by batch/64 so the memory pressure, and hence every request's full offload, is the same
+    **{f"cfg3_b{n}": dict(model="llama3_8b_gqa", hw="b200", pools=(2221882 * n // 64, 2221882 * n // 64 * 8),
+                          layerkv=True, force=-1, max_batch_tokens=n * (32768 + o), trace=("batch", n, 32768, o))
+       for n, o in ((4, 9), (24, 3))},
+    # config 5: block sizes 16/32/64 on the same memory (pools from pool_size_from_hardware at each bs);
+    # the reference's job bytes are token-exact and must not depend on bs (kv_manager.cpp:255-257, 297-299)
+    **{f"cfg5_7b_4k_k{k}_bs{bs}": dict(model="llama2_7b", pools=CFG5_POOLS_7B[bs], bs=bs, layerkv=True,
+                                       force=32 - k, trace=("single", 4096, 65))
+       for k in (1, 16, 32) for bs in (16, 32, 64)},
+    **{f"cfg5_70b_128k_tp8_bs{bs}": dict(model="llama31_70b_gqa", hw="b200", tp=8, nvlink=True,
+                                         pools=CFG5_POOLS_70B[bs], bs=bs, layerkv=True, force=0,
+                                         max_batch_tokens=131072 + 9, trace=("single", 131072, 9))
+       for bs in (16, 32, 64)},
 }
 
 
@@ -60,18 +108,26 @@ def make_trace(lib, spec):
     if kind == "sharegpt":
         _, n, rate, seed = spec
         return drv.generate_trace(lib, True, n, 0, 0, rate, seed)
+    if kind == "batch":  # n requests arriving together at t = 0
+        _, n, p, o = spec
+        return list(range(n)), [0.0] * n, [p] * n, [o] * n
     rows = spec[1]
     return [r[0] for r in rows], [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows]
 
 
+def scenario_hw(sc) -> ls.HardwareSpec:
+    hw = ls.HardwareSpec(**B200_HW) if sc.get("hw") == "b200" else ls.default_hardware()
+    hw.n_gpus = sc.get("tp", 1)
+    hw.nvlink = sc.get("nvlink", hw.nvlink)
+    return hw
+
+
 def scenario_cfg(sc):
     model = getattr(ls, sc["model"])()
-    hw = ls.default_hardware()
-    hw.n_gpus = sc.get("tp", 1)
-    hw.nvlink = sc.get("nvlink", False)
-    return drv.engine_cfg_struct(model, hw, layerkv=sc["layerkv"], slo=sc.get("slo", True),
+    return drv.engine_cfg_struct(model, scenario_hw(sc), layerkv=sc["layerkv"], slo=sc.get("slo", True),
                                  gpu_blocks=sc["pools"][0], cpu_blocks=sc["pools"][1], seed=sc.get("seed", 0),
-                                 force_retained=sc["force"], invariant_checks=sc.get("invariant", False))
+                                 force_retained=sc["force"], invariant_checks=sc.get("invariant", False),
+                                 tpb=sc.get("bs", 16), max_batch_tokens=sc.get("max_batch_tokens", 131072))
 
 
 def engine_goldens(lib):

@@ -31,13 +31,26 @@ def engine_golden():
         return json.load(f)
 
 
+ESCALATIONS = {"te_fcfs_layerkv": 1, "esc_small": 3, "cfg3_b4": 1}
+
+
 # te_contended also passes (261 s: 8.3 TB of re-fetches at the link's 55 GB/s); esc_small and
-# te_fcfs_layerkv cover escalations in seconds.
-@pytest.mark.parametrize("name", ["te_fcfs_layerkv", "esc_small", "cfg1_x16", "cfg1_x0", "te_determinism_baseline",
-                                  "cfg4_tp8"])
-def test_device_virtual_matches_reference_and_bytes(engine_golden, name):
+# te_fcfs_layerkv cover escalations in seconds. (name, tp_rank): the device executes KV-head shard
+# tp_rank of hw.n_gpus — the schedule, and so requests.csv, is the reference's for every shard.
+@pytest.mark.parametrize("name,tp_rank", [
+    ("te_fcfs_layerkv", 0), ("esc_small", 0), ("cfg1_x16", 0), ("cfg1_x0", 0), ("te_determinism_baseline", 0),
+    ("cfg4_tp8", 0),
+    # config 3 (Llama-3-8B GQA, G = 4 on the tcgen05 decode tile): 4 x 32k prompts, every layer offloaded
+    # under the batch-scaled pool, one Full escalation, 8 decode iterations re-fetching 17 GB each
+    ("cfg3_b4", 0),
+    # config 4 on the B200 spec at TP 2 and 4 (last shard of each), TP 8's rank 7
+    ("cfg4_b200_tp2", 1), ("cfg4_b200_tp4", 3), ("cfg4_b200_tp8", 7),
+    # config 5: block sizes 32 / 64 on the 7B half-offloaded 4k case, and 70B 128k fully offloaded at bs 64
+    ("cfg5_7b_4k_k16_bs32", 0), ("cfg5_7b_4k_k16_bs64", 0), ("cfg5_70b_128k_tp8_bs64", 7)])
+def test_device_virtual_matches_reference_and_bytes(engine_golden, name, tp_rank):
     sc = mg.ENGINE_SCENARIOS[name]
-    cfg = serve_cfg(sc, executor="device-virtual", dense_gemms=False, prefill_attention=False, verify_kv=True)
+    cfg = serve_cfg(sc, executor="device-virtual", dense_gemms=False, prefill_attention=False, verify_kv=True,
+                    tp_rank=tp_rank)
     trace = product_trace(sc["trace"])
     summary, rows, csv = serve.run(cfg, trace)
     g = engine_golden[name]
@@ -46,7 +59,7 @@ def test_device_virtual_matches_reference_and_bytes(engine_golden, name):
     assert summary["requests_verified"] == len(trace)
     assert summary["kv_words_mismatched"] == 0
     assert summary["prefills"] == len(trace) and summary["decode_iterations"] > 0
-    assert summary["escalations"] == (1 if name == "te_fcfs_layerkv" else 3 if name == "esc_small" else 0)
+    assert summary["escalations"] == ESCALATIONS.get(name, 0)
 
 
 def test_device_measured_small_trace():

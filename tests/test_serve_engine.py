@@ -35,14 +35,17 @@ def product_trace(spec) -> serve.Trace:
     if kind == "sharegpt":
         _, n, rate, seed = spec
         return serve.generate_sharegpt_like(n, rate, seed)
+    if kind == "batch":
+        _, n, p, o = spec
+        return serve.Trace(list(range(n)), [0.0] * n, [p] * n, [o] * n)
     rows = spec[1]
     return serve.Trace([r[0] for r in rows], [r[1] for r in rows], [r[2] for r in rows], [r[3] for r in rows])
 
 
 def serve_cfg(sc, **kw) -> serve.ServeConfig:
-    hw = ls.default_hardware()
-    hw.n_gpus = sc.get("tp", 1)
-    hw.nvlink = sc.get("nvlink", False)
+    hw = mg.scenario_hw(sc)
+    kw.setdefault("tokens_per_block", sc.get("bs", 16))
+    kw.setdefault("max_batch_tokens", sc.get("max_batch_tokens", 131072))
     return serve.ServeConfig(model=getattr(ls, sc["model"])(), hw=hw, layerkv=sc["layerkv"],
                              slo_scheduler=sc.get("slo", True), gpu_blocks=sc["pools"][0], cpu_blocks=sc["pools"][1],
                              seed=sc.get("seed", 0), force_retained_layers=sc["force"],
