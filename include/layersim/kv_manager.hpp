@@ -28,6 +28,7 @@
 #include <vector>
 
 #include "layersim/cost_model.hpp"
+#include "layersim/errors.hpp"
 
 namespace layersim {
 
@@ -129,8 +130,19 @@ class KvManager {
   ~KvManager() {
     if (observer_) observer_->on_manager_destroyed();
   }
-  KvManager(const KvManager&) = default;
-  KvManager& operator=(const KvManager&) = default;
+  // Copies are plain managers: a bound observer (the device mirror) stays with
+  // the original, and a bound manager cannot be overwritten (its device table
+  // would no longer describe it).
+  KvManager(const KvManager& o)
+      : pools_(o.pools_), n_layers_(o.n_layers_), kvb_(o.kvb_), gpu_(o.gpu_), cpu_(o.cpu_), tables_(o.tables_),
+        pending_(o.pending_), next_job_id_(o.next_job_id_), observer_(nullptr) {}
+  KvManager& operator=(const KvManager& o) {
+    if (this != &o) {
+      if (observer_) throw SimulationError("KvManager: assignment to a manager bound to a device observer");
+      copy_from(o);
+    }
+    return *this;
+  }
 
   int tokens_per_block() const { return pools_.tokens_per_block; }
   std::int64_t gpu_blocks_total() const { return pools_.gpu_blocks_total; }
@@ -229,6 +241,18 @@ class KvManager {
   const Table& table(std::int64_t request_id) const;
   void select_layers(const Table& t, OffloadMode mode, std::vector<int>* out) const;
   std::int64_t filled(const RequestKv& kv, std::size_t block) const;
+
+  void copy_from(const KvManager& o) {
+    pools_ = o.pools_;
+    n_layers_ = o.n_layers_;
+    kvb_ = o.kvb_;
+    gpu_ = o.gpu_;
+    cpu_ = o.cpu_;
+    tables_ = o.tables_;
+    pending_ = o.pending_;
+    next_job_id_ = o.next_job_id_;
+    observer_ = nullptr;
+  }
 
   BlockPools pools_;
   int n_layers_;

@@ -276,7 +276,11 @@ LKV_API int lkv_prefill_layer(lkv_device* dev, int64_t request_id, int32_t layer
  * [tokens][kv_heads_local][head_dim], out [tokens][q_heads_local][head_dim],
  * bf16 on the device, out in out_dtype (LKV_DTYPE_BF16 for serving,
  * LKV_DTYPE_F32 for parity checks); query row i attends keys 0..i. Runs on
- * `stream` (NULL = compute stream). */
+ * `stream` (NULL = compute stream).
+ * Input range: P.V runs in fp16 on an fp16 copy of v. Every bf16 v with
+ * 2^-14 <= |v| <= 65504 converts exactly; smaller values round to fp16
+ * subnormals (absolute error <= 2^-25 per value, so <= 2^-25 on the output);
+ * |v| > 65504 saturates to +-65504 (no inf/NaN). q and k have no limit. */
 LKV_API int lkv_prefill_attention(lkv_device* dev, const void* q, const void* k, const void* v, void* out,
                                   int64_t tokens, float scale, int32_t out_dtype, void* stream);
 /* 1 when the D2H copies of an escalation job have drained. */

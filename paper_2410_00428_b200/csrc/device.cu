@@ -77,10 +77,18 @@ class UploadRing {
     if (bytes > cap_) throw CapacityError("upload ring: request larger than ring");
     if (head_ + bytes > cap_) head_ = 0;
     const std::size_t lo = head_, hi = head_ + bytes;
+    // Retire in FIFO order until NO live region overlaps [lo, hi). After a
+    // wrap the front can be an older region in the skipped tail while a
+    // younger one at the ring's start overlaps, so checking only the front
+    // is not enough.
+    auto overlapping = [&] {
+      for (const Region& r : live_)
+        if (r.lo < hi && lo < r.hi) return true;
+      return false;
+    };
     while (!live_.empty()) {
       const Region& r = live_.front();
-      const bool overlap = r.lo < hi && lo < r.hi;
-      if (!overlap && live_.size() < 4096) break;
+      if (live_.size() < 4096 && !overlapping()) break;
       LKV_CUDA(cudaEventSynchronize(r.ev));
       cudaEventDestroy(r.ev);
       live_.pop_front();
@@ -283,6 +291,8 @@ struct lkv_device final : layersim::KvObserver {
                              cudaHostAllocMapped | cudaHostAllocPortable));
     }
     const long long tbl = static_cast<long long>(cfg.max_requests) * L * cfg.max_blocks;
+    // SeqDesc::row_offset and the snapshot kernel index the table in int32
+    if (tbl > 0x7FFFFFFFll) throw CapacityError("max_requests x n_layers x max_blocks exceeds int32 table indexing");
     LKV_CUDA(cudaMalloc(&d_table, tbl * sizeof(int)));
     LKV_CUDA(cudaMalloc(&d_snap, std::max<long long>(1, static_cast<long long>(L) * cfg.arena_slots) *
                                      sizeof(int)));
@@ -1521,7 +1531,7 @@ int lkv_decode_append_layer(lkv_device* d, int32_t layer, const void* k_new, con
 
 int lkv_decode_layer(lkv_device* d, int32_t layer, const void* q, void* out, float scale,
                      int32_t out_dtype, void* stream) {
-  LKV_REQUIRE(d && q && out);
+  LKV_REQUIRE(d && d->kv && q && out);
   LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
   d->decode_layer(layer, q, out, scale, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<cudaStream_t>(stream));
   LKV_CATCH

@@ -484,10 +484,18 @@ __global__ void fill_kv_kernel(__nv_bfloat16* __restrict__ k, __nv_bfloat16* __r
 }
 
 // bf16 -> fp16, 8 values per thread step (the PF16 prefill attention's V
-// copy). Exact for |x| in fp16's normal range [2^-14, 65504].
+// copy). Exact for |x| in fp16's normal range [2^-14, 65504]; smaller values
+// round to fp16 subnormals (absolute error <= 2^-25), larger ones SATURATE to
+// +-65504 instead of becoming inf (which would turn whole output rows into
+// NaN); NaN stays NaN. The input-range contract is stated on
+// lkv_prefill_attention (include/lkv.h).
 // The prefill attention is launched as its programmatic dependent: it loads
 // Q and K and starts QK^T while this runs, and waits (griddepcontrol.wait)
 // only before its first V load.
+__device__ __forceinline__ float sat_f16(float x) {  // comparisons are false for NaN: it passes through
+  return x > 65504.f ? 65504.f : (x < -65504.f ? -65504.f : x);
+}
+
 __global__ void bf16_to_f16_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, long long n8) {
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n8; i += (long long)gridDim.x * blockDim.x) {
@@ -496,7 +504,8 @@ __global__ void bf16_to_f16_kernel(const uint4* __restrict__ src, uint4* __restr
     uint32_t o[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const __half2 h = __floats2half2_rn(__uint_as_float(w[j] << 16), __uint_as_float(w[j] & 0xFFFF0000u));
+      const __half2 h = __floats2half2_rn(sat_f16(__uint_as_float(w[j] << 16)),
+                                          sat_f16(__uint_as_float(w[j] & 0xFFFF0000u)));
       o[j] = *reinterpret_cast<const uint32_t*>(&h);
     }
     dst[i] = make_uint4(o[0], o[1], o[2], o[3]);

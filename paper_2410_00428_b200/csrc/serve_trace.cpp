@@ -113,7 +113,7 @@ namespace {
 // strings, true/false/null. Nested values are rejected.
 struct FlatObject {
   struct Val {
-    enum Kind { Number, String, Bool, Null } kind;
+    enum Kind { Number, String, Bool, Null, Nested } kind;
     std::string text;
     bool is_integer = false;
   };
@@ -169,6 +169,22 @@ std::string parse_string(Cursor& c) {
   return out;
 }
 
+// Skips one array or object value (brackets matched, strings respected).
+void skip_nested(Cursor& c) {
+  int depth = 0;
+  do {
+    if (c.p >= c.end) throw std::runtime_error("unterminated array/object");
+    const char ch = *c.p;
+    if (ch == '"') {
+      parse_string(c);
+      continue;
+    }
+    if (ch == '[' || ch == '{') ++depth;
+    if (ch == ']' || ch == '}') --depth;
+    ++c.p;
+  } while (depth > 0);
+}
+
 FlatObject parse_object(const std::string& line) {
   Cursor c{line.data(), line.data() + line.size()};
   FlatObject obj;
@@ -192,6 +208,9 @@ FlatObject parse_object(const std::string& line) {
         c.p += 5;
       } else if (c.end - c.p >= 4 && std::strncmp(c.p, "null", 4) == 0) {
         c.p += 4;
+      } else if (c.p < c.end && (*c.p == '[' || *c.p == '{')) {
+        skip_nested(c);  // extra array/object fields are ignored, as the reference's nlohmann reader does
+        v.kind = FlatObject::Val::Nested;
       } else {
         const char* s = c.p;
         if (c.p < c.end && *c.p == '-') ++c.p;

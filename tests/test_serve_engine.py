@@ -124,6 +124,27 @@ def test_reference_reads_product_jsonl(ref, tmp_path):
     assert back == t
 
 
+def test_jsonl_ignores_nested_extra_fields(ref, tmp_path):
+    """Extra array / object fields (metadata) are ignored, as the reference's
+    nlohmann-based load_trace ignores them (workload.cpp:84-136)."""
+    body = ('{"id": 3, "tags": ["a", "]}", {"x": [1, 2]}], "arrival_s": 0.5, "meta": {"k": {"z": "}"}, "n": null}, '
+            '"prompt_tokens": 7, "output_tokens": 2}\n'
+            '{"meta": [], "id": 4, "arrival_s": 1.25, "prompt_tokens": 9, "output_tokens": 1, "o": {}}\n')
+    p = tmp_path / "nested.jsonl"
+    p.write_text(body)
+    back, unsorted = serve.load_trace(p)
+    assert not unsorted and (back.ids, back.arrival, back.prompt, back.output) == ([3, 4], [0.5, 1.25], [7, 9], [2, 1])
+    if hasattr(ref.dll, "ref_load_trace"):
+        import ctypes as C
+        ids, arr, pr, o = (C.c_int64 * 2)(), (C.c_double * 2)(), (C.c_int32 * 2)(), (C.c_int32 * 2)()
+        assert ref.dll.ref_load_trace(str(p).encode(), ids, arr, pr, o, 2) == 2
+        assert (list(ids), list(arr), list(pr), list(o)) == (back.ids, back.arrival, back.prompt, back.output)
+    bad = tmp_path / "bad_nested.jsonl"
+    bad.write_text('{"id": 1, "arrival_s": 0, "prompt_tokens": 2, "output_tokens": 1, "t": [1, 2\n')
+    with pytest.raises(ls.LkvError, match="parse error"):
+        serve.load_trace(bad)
+
+
 def test_errors_are_loud():
     sc = mg.ENGINE_SCENARIOS["te_fcfs_layerkv"]
     cfg = serve_cfg(sc)
