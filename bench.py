@@ -158,93 +158,60 @@ def host_link_peak(torch, dev):
     return out
 
 
-# ------------------------------------------------------------------ CPU port
-def cpu_port(host_pool_ptr, slots_per_layer, slot_bytes, kv_len, hkv, group, bs, d, seconds, max_layers=None):
-    """Oracle CPU port of the decode step (see oracle/cpu_baseline.c)."""
-    import ctypes as C
-    import numpy as np
-    import oracle
-    re = oracle.restatement()
-    fn = re.dll.cpu_decode_layer
-    fn.restype = None
-    fn.argtypes = [C.c_void_p, C.c_void_p, C.c_int, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
-                   C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_int]
-    threads = os.cpu_count() or 1
-    nblk = len(slots_per_layer[0])
-    arena = np.empty(nblk * slot_bytes, np.uint8)
-    q = (np.random.default_rng(0).random((hkv * group, d), dtype=np.float32) * 2 - 1)
-    q16 = (q.view(np.uint32) >> 16).astype(np.uint16)
-    out = np.empty((hkv * group, d), np.float32)
-    rows = [np.asarray(s, np.uint32) for s in slots_per_layer]
-    t0 = time.perf_counter()
-    done = 0
-    while True:  # whole passes over the given layers until the time budget is spent
-        for s in rows:
-            fn(host_pool_ptr, s.ctypes.data, nblk, slot_bytes, kv_len, hkv, group, bs, d, q16.ctypes.data,
-               1.0 / math.sqrt(d), out.ctypes.data, arena.ctypes.data, threads)
-            done += 1
-            if max_layers and done >= max_layers:
-                break
-        if (max_layers and done >= max_layers) or time.perf_counter() - t0 > seconds:
-            break
-    dt = time.perf_counter() - t0
-    kv_bytes = done * kv_len * 2 * hkv * d * 2
-    return kv_bytes / dt / 1e9, threads, done, dt
-
-
+# ------------------------------------------------------------------ CPU reference arm
 def reference_arm(args):
-    """`--impl reference`: rank 0 alone runs the reference's CPU path."""
+    """`--impl reference`: rank 0 alone runs the reference's CPU path — the
+    REFERENCE KvManager (oracle/_ref, compiled in place from /root/reference)
+    books every member's decode fetch (plan_decode_fetch, kv_manager.cpp:
+    290-304), and the oracle CPU port (oracle/ref_arm.Port, the same code the
+    product line's cpu_baseline leg times) executes it: memcpy of each
+    layer's slots into an arena + fp32 attention, on all host threads. This
+    arm imports nothing from the product package."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    import ctypes as C
     import numpy as np
-    import oracle
-    from paper_2410_00428_b200 import layersim as ls
-    model = ls.llama2_7b()
-    L, bs, d = model.n_layers, 16, model.d_head
-    lib = oracle.ref_lib() if oracle.ref_available() else None
-    kind_book = "reference" if lib is not None else "product"
-    kv = ls.KvManager(ls.BlockPools(113043, 904344, bs), model, lib=lib)
+    from oracle import ref_arm
+    L, bs, d, hkv = 32, 16, 128, 32
+    kv = ref_arm.RefKvManager(113043, 904344, bs)
     B = args.batch
     for rid in range(B):
         assert kv.allocate_prefill(rid, args.ctx, args.retained)
     nblk = (args.ctx + bs - 1) // bs
-    slot_bytes = 2 * model.n_kv_heads * bs * d * 2
+    slot_bytes = 2 * hkv * bs * d * 2
     # Host frames: the step reads B x 32 x 1024 distinct slots (60 GB at 16k);
-    # the sample maps them modulo a 4 GiB frame pool (>> LLC, so every read
-    # still comes from DRAM) with synthetic bf16 values.
+    # they are mapped modulo a 4 GiB frame pool (>> LLC, so every read still
+    # comes from DRAM), touched once, with synthetic bf16 values.
     frames = (4 << 30) // slot_bytes
     pool = np.random.default_rng(1).integers(0x3C00, 0x3F80, size=frames * slot_bytes // 2, dtype=np.uint16)
     pool[::2] ^= 0x8000
-    tables = []
-    for rid in range(B):
-        r = kv.request(rid)
-        tables.append([[r.blocks[b].layers[l].slot % frames for b in range(nblk)] for l in range(L)])
+    tables = [[np.asarray([s % frames for s in row], np.uint32) for row in kv.slots(rid)] for rid in range(B)]
+    port = ref_arm.Port(nblk, slot_bytes, args.ctx, hkv, 1, bs, d)
     steps = []
-    cores = os.cpu_count() or 1
     for i in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        for rid in range(B):  # one decode iteration: every member, every layer
+        for rid in range(B):  # one decode iteration: every member, every CPU-resident layer
             jobs = kv.plan_decode_fetch(rid)  # the reference's own booking of this step
             assert len(jobs) == L - args.retained
-            cpu_port(pool.ctypes.data, tables[rid], slot_bytes, args.ctx, model.n_kv_heads, 1, bs, d, 0.0,
-                     max_layers=L)
+            for layer, _ in jobs:
+                port.layer(pool.ctypes.data, tables[rid][layer])
         step = time.perf_counter() - t0
         if i >= args.warmup:
             steps.append(step)
-    S = L
-    step_bytes = B * S * args.ctx * ls.kv_bytes_per_token_layer(model)
+    kv.close()
+    step_bytes = B * (L - args.retained) * args.ctx * ref_arm.kv_bytes_per_token_layer()
     ms = 1000 * statistics.mean(steps)
     value = step_bytes / (ms / 1000) / 1e9
-    sample = (f"full decode iteration per step ({B} requests x 32 layers x {args.ctx} tokens, 7B shape): "
-              f"{kind_book} bookkeeping (plan_decode_fetch) + oracle CPU port memcpy prefetch + fp32 attention; "
-              f"frames mapped modulo a 4 GiB pool")
+    sample = (f"full decode iteration per step ({B} requests x {L - args.retained} CPU-resident layers x {args.ctx} "
+              f"tokens, 7B shape): reference KvManager bookkeeping (plan_decode_fetch, oracle/_ref) + oracle CPU port "
+              f"(oracle/ref_arm.Port) memcpy prefetch + fp32 attention, {port.threads} threads; frames mapped modulo "
+              f"a 4 GiB pool")
     line = {"metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "config": workload_config(args),
             "impl": "reference",
-            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": cores, "kind": "port", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GB/s", "cores": port.threads, "kind": "port",
+                             "sample": sample},
             "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "host": host_info()}
     print(json.dumps(line), flush=True)
@@ -915,13 +882,14 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        r = kv.request(0)
-        slots = [[r.blocks[b].layers[l].slot for b in range(nblk)] for l in range(L)]
-        gbs, cores, done, dt = cpu_port(dev.info.host_pool, slots, dev.slot_bytes, ctx, hl, hql // hl, bs, d,
-                                        args.cpu_seconds)
-        cpu = {"value": gbs, "unit": "GB/s", "cores": cores, "kind": "port",
-               "sample": f"{done} (request 0, layer) decode passes over the same pinned frames ({ctx} tokens "
-                         f"each, {dt:.1f} s): oracle CPU port memcpy prefetch + fp32 attention, {cores} threads"}
+        from oracle import ref_arm  # the checker / CPU baseline only, after the timed region
+        slots = [[kv.request(rid).blocks[b].layers[l].slot for b in range(nblk)] for rid in ids for l in range(L)]
+        port = ref_arm.Port(nblk, dev.slot_bytes, ctx, hl, hql // hl, bs, d)
+        gbs, done, dt = port.timed(dev.info.host_pool, slots, args.cpu_seconds)
+        cpu = {"value": gbs, "unit": "GB/s", "cores": port.threads, "kind": "port",
+               "sample": f"{done} (request, layer) decode passes over the same pinned frames ({ctx} tokens each, "
+                         f"{dt:.1f} s): oracle CPU port (oracle/ref_arm.Port, the --impl reference arm's code) "
+                         f"memcpy prefetch + fp32 attention, {port.threads} threads"}
 
     if rank == 0:
         line = {

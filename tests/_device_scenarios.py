@@ -57,8 +57,47 @@ def random_q(n, hq, d, gen_seed):
     return (torch.rand((n, hq, d), generator=g) * 2 - 1).to(torch.bfloat16)
 
 
-def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=None, tol=None):
-    """One decode iteration over `ids`; every layer compared with the oracle."""
+def peaked_q(dev, layer, kv_lens, mode, seed=SEED, gen_seed=0):
+    """Queries whose softmax is far from uniform, so the running-max paths run
+    on their non-trivial branches (decode_gqa_tc.cuh lazy max, the split
+    merge's rescale).
+
+    mode "scaled": random q x 16 — scores of std ~5 (natural units) instead
+    of ~0.3, so each 128-token tile has its own maximum.
+    mode "rising": each query head is a weighted sum of the generator's keys
+    at 4 anchor tokens (10%, 40%, 75%, 97% of the sequence) with weights
+    2, 5, 8, 11: the scaled scores at the anchors are ~7.6, 19, 30 and 42
+    against a background of std ~5, so the running maximum jumps by ~11
+    (~16 in log2, past kLazyMax = 8) at tiles and chunks deep in the
+    sequence, and the output is dominated by the last anchor's V.
+    mode "extreme": weights 5, 15, 25, 35 — the anchors' scores rise by
+    ~165 in log2 over the sequence, past fp32's exponent range, so a kernel
+    that stopped re-basing its running maximum would overflow."""
+    import torch
+    import oracle
+    n = len(kv_lens)
+    hq, hl, d = dev.q_heads_local, dev.kv_heads_local, dev.head_dim
+    group = hq // hl
+    coef = (5.0, 15.0, 25.0, 35.0) if mode == "extreme" else (2.0, 5.0, 8.0, 11.0)
+    if mode == "scaled":
+        return (random_q(n, hq, d, 2000 + layer + gen_seed).float() * 16).to(torch.bfloat16)
+    re = oracle.restatement()
+    g = np.random.default_rng(3000 + layer + gen_seed)
+    q = np.zeros((n, hq, d), np.float32)
+    for m, kv_len in enumerate(kv_lens):
+        anchors = sorted({min(kv_len - 1, int(kv_len * f)) for f in (0.10, 0.40, 0.75, 0.97)})
+        for i, t in enumerate(anchors):
+            k, _ = re.fill_kv(1, t, layer, hl, dev.head0, d, seed)
+            kf = (k.astype(np.uint32) << 16).view(np.float32)[0]  # [hl][d]
+            c = coef[i + 4 - len(anchors)]
+            q[m] += c * np.repeat(kf, group, axis=0)
+        q[m] += g.uniform(-0.25, 0.25, size=(hq, d))
+    return torch.from_numpy(q).to(torch.bfloat16)
+
+
+def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=None, tol=None, q_mode=None):
+    """One decode iteration over `ids`; every layer compared with the oracle.
+    q_mode: None = U(-1, 1) queries; "scaled" / "rising" = peaked_q."""
     import torch
     import oracle
     re = oracle.restatement()
@@ -67,7 +106,8 @@ def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=No
     group = hq // dev.kv_heads_local
     scale = 1.0 / math.sqrt(d)
     L = dev.model.n_layers
-    qs = [random_q(n, hq, d, 1000 + l) for l in range(L)]
+    qs = [random_q(n, hq, d, 1000 + l) if q_mode is None else peaked_q(dev, l, kv_lens, q_mode, seed)
+          for l in range(L)]
     outs = []
     dev.decode_begin(ids)
     for l in range(L):

@@ -66,3 +66,17 @@ def test_reference_arm_contract():
     line = _last_json(r.stdout)
     assert line["impl"] == "reference"
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["cores"] >= 1
+
+
+def test_reference_arm_loads_no_product_code():
+    """The reference arm neither imports the product package nor maps liblkv.so."""
+    code = ("import runpy, sys\n"
+            "sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0', '--batch', '1',"
+            " '--ctx', '512']\n"
+            "runpy.run_path('bench.py', run_name='__main__')\n"
+            "maps = open('/proc/self/maps').read()\n"
+            "print('PRODUCT_MODULES', [m for m in sys.modules if m.startswith('paper_2410_00428_b200')])\n"
+            "print('LIBLKV_MAPPED', 'liblkv.so' in maps, 'libref_layersim.so' in maps)\n")
+    r = subprocess.run([sys.executable, "-c", code], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "PRODUCT_MODULES []" in r.stdout and "LIBLKV_MAPPED False True" in r.stdout, r.stdout[-500:]

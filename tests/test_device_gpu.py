@@ -122,6 +122,40 @@ def test_attention_parity_each_merge(merge, group, monkeypatch):
     sc.check_attention(dev, list(range(len(lens))), lens)
 
 
+@pytest.mark.parametrize("mode", ["scaled", "rising", "extreme"])
+@pytest.mark.parametrize("group,bs", [(1, 16), (2, 16), (4, 16), (8, 16), (4, 64)])
+def test_attention_parity_peaked_softmax(mode, group, bs):
+    """Peaked softmax (tests/_device_scenarios.peaked_q): scores whose running
+    maximum rises tile after tile and chunk after chunk, so the tcgen05 tile's
+    lazy max (decode_gqa_tc.cuh, raise when s > m_run + kLazyMax) fires mid
+    sequence with its O/l correction, and the split merge rescales partials
+    of different maxima. Lengths from 1 token to 40 chunks; some requests
+    CPU-resident (arena frames)."""
+    model = sc.gqa_model(L=2, hkv=4 if group < 8 else 2, group=group)
+    kv, dev = sc.make(model, bs=bs, gpu=6000, cpu=6000, max_blocks=1400, arena=6000)
+    lens = [1, 100, 129, 700, 5000, 20000]
+    for rid, n in enumerate(lens):
+        sc.prefill(kv, dev, rid, n, rid % 3)
+    sc.check_attention(dev, list(range(len(lens))), lens, q_mode=mode)
+    dev.close()
+
+
+@pytest.mark.parametrize("mode", [None, "rising"])
+def test_attention_parity_bench_shape_g1(mode):
+    """The headline's shape: LLaMA-2-7B heads (Hkv = Hq = 32, G = 1, the
+    CUDA-core decode_attn_v2 kernel), 7 x 16384 tokens, every layer
+    CPU-resident (x = 0, prefetched into the arena), all 32 heads of the last
+    layer against the oracle."""
+    model = ls.ModelSpec(2, 32, 32, 128, 4096, 7e9, 2)
+    B, T, nblk = 7, 16384, 1024
+    kv, dev = sc.make(model, gpu=64, cpu=B * nblk * 2 + 64, max_blocks=nblk + 8, max_batch=B,
+                      arena=B * nblk + 16, chunk_slots=64)
+    for rid in range(B):
+        sc.prefill(kv, dev, rid, T, 0)
+    sc.check_attention(dev, list(range(B)), [T] * B, layers=[1], q_mode=mode)
+    dev.close()
+
+
 def test_attention_bf16_output():
     model = sc.gqa_model(L=2, hkv=8, group=4)
     kv, dev = sc.make(model)
