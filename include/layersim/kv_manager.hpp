@@ -195,6 +195,19 @@ class KvManager {
   // Token-exact bytes of CPU-resident KV of layer `layer` (the per-layer
   // plan_decode_fetch value, 0 when nothing is on the CPU).
   std::int64_t cpu_layer_bytes(std::int64_t request_id, int layer) const;
+  // Free-list journal for the device mirror. A LIFO stack
+  // (kv_manager.cpp:52-74) is [total-1 ... next_fresh] + pushed[0..size):
+  // between two takes, pops only shrink `pushed` to a low-water mark and
+  // pushes append above it, so the change is (next_fresh, low, size,
+  // pushed[low..size)). `full` restarts from low = 0.
+  struct FreeListDelta {
+    std::int64_t next_fresh = 0, low = 0, size = 0;
+    const std::uint32_t* pushed = nullptr;  // the whole pushed stack; entries [low, size) changed
+    bool changed = false;
+  };
+  FreeListDelta take_free_delta(bool gpu, bool full = false);
+  // The stack itself: next_fresh and the pushed part (top = back).
+  void free_stack(bool gpu, std::int64_t* next_fresh, std::vector<std::uint32_t>* pushed) const;
 
  private:
   // LIFO slot stack. The reference seeds its stack with total-1 ... 0 so the
@@ -212,12 +225,17 @@ class KvManager {
     }
     bool held(std::uint32_t slot) const;
     std::int64_t high_water() const { return next_fresh_; }
+    FreeListDelta take_delta(bool full);
+    const std::vector<std::uint32_t>& pushed() const { return pushed_; }
 
    private:
     std::int64_t total_;
     std::int64_t next_fresh_ = 0;
     std::vector<std::uint32_t> pushed_;
     std::vector<std::uint64_t> held_bits_;  // grows with next_fresh_
+    // journal state of the device mirror: lowest pushed_.size() and
+    // next_fresh_ since the last take_delta
+    std::int64_t low_ = 0, fresh_taken_ = 0;
   };
 
   struct Table {

@@ -171,6 +171,11 @@ LKV_API int lkv_kv_check_conservation(const lkv_kv_manager*);
 LKV_API int lkv_kv_dump_table(const lkv_kv_manager*, char* buf, size_t cap, size_t* len);
 /* FNV-1a-64 of the dump_table text (the parity hash of BASELINE.md §2). */
 LKV_API int lkv_kv_dump_hash(const lkv_kv_manager*, uint64_t* out);
+/* One LIFO free list (which: 0 = GPU, 1 = CPU) as the reference's SlotPool
+ * keeps it (free_stack_, kv_manager.hpp:153-166, kv_manager.cpp:52-74): the
+ * whole stack bottom to top (next alloc = last). *size = free slots; the stack
+ * is written to out when cap >= *size. */
+LKV_API int lkv_kv_free_stack(const lkv_kv_manager*, int32_t which, uint32_t* out, int64_t cap, int64_t* size);
 
 /* ---- PcieBus, parity-mode timing (reference interconnect.hpp:9-80) ------ */
 typedef struct lkv_pcie_bus lkv_pcie_bus;
@@ -403,6 +408,9 @@ LKV_API int lkv_verify_request(lkv_device* dev, int64_t request_id, int64_t n_to
 /* One CPU slot's bytes (slot_bytes) into dst, wherever they live (pinned
  * frame or pageable home); waits for in-flight copies into it. */
 LKV_API int lkv_device_read_host_slot(lkv_device* dev, int64_t cpu_slot, void* dst);
+/* The device mirror of one free list, read back from HBM after pending
+ * journal updates are applied, in lkv_kv_free_stack's form. */
+LKV_API int lkv_device_free_stack(lkv_device* dev, int32_t which, uint32_t* out, int64_t cap, int64_t* size);
 typedef struct lkv_host_tier_stats {
   int64_t pinned_frames, read_in_frames, write_back_frames, evictions, hits, misses;
 } lkv_host_tier_stats;

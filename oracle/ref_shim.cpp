@@ -82,6 +82,26 @@ OffloadMode mode_of(int32_t m) { return m == LKV_OFFLOAD_HALF ? OffloadMode::Hal
   }                \
   return LKV_OK;
 
+#ifndef LKV_SHIM_HYBRID
+// Reference build: read the private SlotPool::free_stack_ (kv_manager.hpp:
+// 153-166) without touching the reference headers. Names in an explicit
+// instantiation are exempt from access checking, and the friend each
+// instantiation defines returns the member pointer; `auto` avoids naming the
+// private types anywhere else.
+namespace {
+struct GpuPoolTag { friend auto rob(GpuPoolTag); };
+struct CpuPoolTag { friend auto rob(CpuPoolTag); };
+struct StackTag { friend auto rob(StackTag); };
+template <typename Tag, auto P>
+struct Rob {
+  friend auto rob(Tag) { return P; }
+};
+template struct Rob<GpuPoolTag, &KvManager::gpu_>;
+template struct Rob<CpuPoolTag, &KvManager::cpu_>;
+template struct Rob<StackTag, &KvManager::SlotPool::free_stack_>;
+}  // namespace
+#endif
+
 extern "C" {
 
 const char* lkv_last_error(void) { return g_err.c_str(); }
@@ -225,6 +245,30 @@ int lkv_kv_dump_table(const lkv_kv_manager* k, char* buf, size_t cap, size_t* le
   }
   CATCH
 }
+#ifdef LKV_SHIM_HYBRID
+// hybrid: the product KvManager (its public free_stack)
+int lkv_kv_free_stack(const lkv_kv_manager* k, int32_t which, uint32_t* out, int64_t cap, int64_t* size) {
+  TRY std::int64_t fresh = 0;
+  std::vector<std::uint32_t> pushed;
+  k->impl.free_stack(which == 0, &fresh, &pushed);
+  const std::int64_t total = which == 0 ? k->impl.gpu_blocks_total() : k->impl.cpu_blocks_total();
+  *size = (total - fresh) + static_cast<std::int64_t>(pushed.size());
+  if (cap >= *size) {
+    for (std::int64_t i = 0; i < total - fresh; ++i) out[i] = static_cast<std::uint32_t>(total - 1 - i);
+    std::copy(pushed.begin(), pushed.end(), out + (total - fresh));
+  }
+  CATCH
+}
+#else
+int lkv_kv_free_stack(const lkv_kv_manager* k, int32_t which, uint32_t* out, int64_t cap, int64_t* size) {
+  TRY const auto& pool = which == 0 ? k->impl.*rob(GpuPoolTag{}) : k->impl.*rob(CpuPoolTag{});
+  const std::vector<std::uint32_t>& st = pool.*rob(StackTag{});
+  *size = static_cast<int64_t>(st.size());
+  if (cap >= *size) std::copy(st.begin(), st.end(), out);
+  CATCH
+}
+#endif
+
 int lkv_kv_dump_hash(const lkv_kv_manager* k, uint64_t* o) {
   TRY std::ostringstream os;
   k->impl.dump_table(os);

@@ -164,6 +164,7 @@ _PROTOS = {
     "lkv_kv_check_conservation": [vp],
     "lkv_kv_dump_table": [vp, C.c_char_p, C.c_size_t, P(C.c_size_t)],
     "lkv_kv_dump_hash": [vp, P(u64)],
+    "lkv_kv_free_stack": [vp, i32, P(u32), i64, P(i64)],
     "lkv_bus_create": [f64, P(vp)],
     "lkv_bus_destroy": [vp],
     "lkv_bus_register_allreduce": [vp, f64, f64, P(HardwareSpec)],
@@ -209,6 +210,7 @@ _PROTOS = {
     "lkv_verify_request": [vp, i64, i64, u64, P(i64)],
     "lkv_fill_request": [vp, i64, i64, u64],
     "lkv_device_read_host_slot": [vp, i64, vp],
+    "lkv_device_free_stack": [vp, i32, P(u32), i64, P(i64)],
     "lkv_device_host_tier_stats": [vp, P(HostTierStats)],
 }
 _RET = {"lkv_last_error": C.c_char_p, "lkv_version": C.c_char_p}

@@ -404,6 +404,20 @@ int lkv_kv_dump_table(const lkv_kv_manager* kv, char* buf, size_t cap, size_t* l
   LKV_CATCH
 }
 
+int lkv_kv_free_stack(const lkv_kv_manager* kv, int32_t which, uint32_t* out, int64_t cap, int64_t* size) {
+  LKV_REQUIRE(kv && (which == 0 || which == 1) && size && (out || cap == 0));
+  LKV_TRY std::int64_t fresh = 0;
+  std::vector<std::uint32_t> pushed;
+  kv->impl.free_stack(which == 0, &fresh, &pushed);
+  const std::int64_t total = which == 0 ? kv->impl.gpu_blocks_total() : kv->impl.cpu_blocks_total();
+  *size = (total - fresh) + static_cast<std::int64_t>(pushed.size());
+  if (cap >= *size) {
+    for (std::int64_t i = 0; i < total - fresh; ++i) out[i] = static_cast<std::uint32_t>(total - 1 - i);
+    std::copy(pushed.begin(), pushed.end(), out + (total - fresh));
+  }
+  LKV_CATCH
+}
+
 int lkv_kv_dump_hash(const lkv_kv_manager* kv, uint64_t* out) {
   LKV_REQUIRE(kv && out);
   LKV_TRY std::ostringstream os;

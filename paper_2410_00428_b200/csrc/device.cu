@@ -153,6 +153,10 @@ struct lkv_device final : layersim::KvObserver {
     tier.used(slots.data(), static_cast<long long>(slots.size()), ev, write);  // takes the event
   }
   int* d_table = nullptr;      // [max_requests][L][max_blocks]
+  unsigned* d_free_gpu = nullptr;   // free-list mirror (FreeSync): pushed part of the GPU stack, [gpu_slots]
+  unsigned* d_free_cpu = nullptr;   // ... of the CPU stack, [host_slots]
+  long long* d_free_hdr = nullptr;  // [2][3] {total, next_fresh, pushed size}
+  bool free_full = true;            // next flush uploads both stacks whole (bind)
   int* d_snap = nullptr;       // [L][arena_slots]
   unsigned long long* d_stamps = nullptr;  // timing: [L][2] attention kernel span (%globaltimer min start, max end)
   unsigned long long* layer_stamps(int l) { return timing && d_stamps ? d_stamps + 2 * l : nullptr; }
@@ -294,6 +298,9 @@ struct lkv_device final : layersim::KvObserver {
     // SeqDesc::row_offset and the snapshot kernel index the table in int32
     if (tbl > 0x7FFFFFFFll) throw CapacityError("max_requests x n_layers x max_blocks exceeds int32 table indexing");
     LKV_CUDA(cudaMalloc(&d_table, tbl * sizeof(int)));
+    LKV_CUDA(cudaMalloc(&d_free_gpu, std::max<long long>(1, cfg.gpu_slots) * sizeof(unsigned)));
+    LKV_CUDA(cudaMalloc(&d_free_cpu, std::max<long long>(1, cfg.host_slots) * sizeof(unsigned)));
+    LKV_CUDA(cudaMalloc(&d_free_hdr, 6 * sizeof(long long)));
     LKV_CUDA(cudaMalloc(&d_snap, std::max<long long>(1, static_cast<long long>(L) * cfg.arena_slots) *
                                      sizeof(int)));
     LKV_CUDA(cudaMalloc(&d_seqs, cfg.max_batch * sizeof(SeqDesc)));
@@ -336,6 +343,7 @@ struct lkv_device final : layersim::KvObserver {
     // stream (a legacy-stream memset would race the non-blocking streams).
     LKV_CUDA(cudaMemsetAsync(dbuf, 0, std::max<long long>(frames, 1) * sb, cs));
     LKV_CUDA(cudaMemsetAsync(d_table, 0, tbl * sizeof(int), cs));
+    LKV_CUDA(cudaMemsetAsync(d_free_hdr, 0, 6 * sizeof(long long), cs));
     LKV_CUDA(cudaStreamSynchronize(cs));
     seg_ready.resize(cfg.staging_chunks);
     seg_free.resize(cfg.staging_chunks);
@@ -405,6 +413,9 @@ struct lkv_device final : layersim::KvObserver {
     tier.destroy();
     cudaFree(d_xlat);
     cudaFree(d_table);
+    cudaFree(d_free_gpu);
+    cudaFree(d_free_cpu);
+    cudaFree(d_free_hdr);
     cudaFree(d_snap);
     cudaFree(d_stamps);
     cudaFree(d_seqs);
@@ -466,15 +477,54 @@ struct lkv_device final : layersim::KvObserver {
     journal.resize(w);
   }
 
+  // Applies the table journal and the free lists' changes (the device mirror
+  // of the manager's state) with one kernel on the
+  // compute stream, ahead of any consumer.
   void flush() {
-    if (journal.empty()) return;
+    FreeSync fs{};
+    KvManager::FreeListDelta fd[2];
+    if (kv) {
+      for (int l = 0; l < 2; ++l) {
+        fd[l] = kv->take_free_delta(l == 0, free_full);
+        const long long cap = l == 0 ? cfg.gpu_slots : cfg.host_slots;
+        if (fd[l].size > cap)
+          throw CapacityError("device free-list mirror: " + std::to_string(fd[l].size) + " free " +
+                              (l == 0 ? "GPU" : "CPU") + " slots > " + std::to_string(cap) + " frames");
+        if (fd[l].changed) fs.any = 1;
+      }
+      free_full = false;
+    }
+    if (journal.empty() && !fs.any) return;
     dedupe_journal();
     const std::size_t n = journal.size();
-    auto* dst = reinterpret_cast<TableUpdate*>(ring.reserve(n * sizeof(TableUpdate)));
-    std::memcpy(dst, journal.data(), n * sizeof(TableUpdate));
+    const std::size_t tbytes = (n * sizeof(TableUpdate) + 15) & ~std::size_t(15);
+    std::size_t fbytes[2] = {0, 0};
+    if (fs.any)
+      for (int l = 0; l < 2; ++l) fbytes[l] = ((fd[l].size - fd[l].low) * sizeof(unsigned) + 15) & ~std::size_t(15);
+    char* up = ring.reserve(std::max<std::size_t>(16, tbytes + fbytes[0] + fbytes[1]));
+    auto* dst = reinterpret_cast<TableUpdate*>(up);
+    if (n) std::memcpy(dst, journal.data(), n * sizeof(TableUpdate));
+    long long work = static_cast<long long>(n);
+    if (fs.any) {
+      char* p = up + tbytes;
+      for (int l = 0; l < 2; ++l) {
+        const long long cnt = fd[l].size - fd[l].low;
+        if (cnt) std::memcpy(p, fd[l].pushed + fd[l].low, cnt * sizeof(unsigned));
+        fs.src[l] = reinterpret_cast<const unsigned*>(p);
+        fs.dst[l] = l == 0 ? d_free_gpu : d_free_cpu;
+        fs.low[l] = fd[l].low;
+        fs.n[l] = cnt;
+        fs.total[l] = l == 0 ? kv->gpu_blocks_total() : kv->cpu_blocks_total();
+        fs.fresh[l] = fd[l].next_fresh;
+        fs.size[l] = fd[l].size;
+        work = std::max(work, cnt);
+        p += fbytes[l];
+      }
+      fs.hdr = d_free_hdr;
+    }
     const int threads = 256;
-    const int grid = static_cast<int>(std::min<std::size_t>((n + threads - 1) / threads, 4 * sms));
-    table_apply_kernel<<<grid, threads, 0, cs>>>(dst, static_cast<int>(n), d_table);
+    const int grid = static_cast<int>(std::clamp<long long>((work + threads - 1) / threads, 1, 4ll * sms));
+    table_apply_kernel<<<grid, threads, 0, cs>>>(dst, static_cast<int>(n), d_table, fs);
     LKV_CUDA(cudaGetLastError());
     ring.commit(cs);
     journal.clear();
@@ -1314,6 +1364,7 @@ void device_bind_manager(lkv_device* d, KvManager& k) {
   if (k.tokens_per_block() != d->bs) throw std::invalid_argument("bind: tokens_per_block mismatch");
   if (!k.request_ids().empty()) throw std::invalid_argument("bind: manager already holds requests");
   d->kv = &k;
+  d->free_full = true;
   k.set_observer(d);
 }
 // Completion event of an escalation job's last D2H copy (timing-capable);
@@ -1722,7 +1773,7 @@ static void request_pass(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t s
       if (!slots.empty()) {
         auto* up = reinterpret_cast<TableUpdate*>(d->ring.reserve(slots.size() * sizeof(TableUpdate)));
         for (std::size_t i = 0; i < slots.size(); ++i) up[i] = {slots[i], static_cast<int>(frames[i]), 0};
-        table_apply_kernel<<<1, 256, 0, d->cs>>>(up, static_cast<int>(slots.size()), d->d_xlat);
+        table_apply_kernel<<<1, 256, 0, d->cs>>>(up, static_cast<int>(slots.size()), d->d_xlat, FreeSync{});
         LKV_CUDA(cudaGetLastError());
         d->ring.commit(d->cs);
       }
@@ -1749,6 +1800,26 @@ static void request_pass(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t s
   } else {
     LKV_CUDA(cudaStreamSynchronize(d->cs));
   }
+}
+
+int lkv_device_free_stack(lkv_device* d, int32_t which, uint32_t* out, int64_t cap, int64_t* size) {
+  LKV_REQUIRE(d && (which == 0 || which == 1) && size && (out || cap == 0));
+  LKV_TRY LKV_CUDA(cudaSetDevice(d->cfg.device));
+  d->flush();
+  long long hdr[6];
+  LKV_CUDA(cudaMemcpyAsync(hdr, d->d_free_hdr, sizeof hdr, cudaMemcpyDeviceToHost, d->cs));
+  LKV_CUDA(cudaStreamSynchronize(d->cs));
+  const long long total = hdr[3 * which], fresh = hdr[3 * which + 1], pushed = hdr[3 * which + 2];
+  *size = (total - fresh) + pushed;
+  if (cap >= *size) {
+    for (long long i = 0; i < total - fresh; ++i) out[i] = static_cast<uint32_t>(total - 1 - i);
+    if (pushed > 0) {
+      LKV_CUDA(cudaMemcpyAsync(out + (total - fresh), which == 0 ? d->d_free_gpu : d->d_free_cpu,
+                               pushed * sizeof(unsigned), cudaMemcpyDeviceToHost, d->cs));
+      LKV_CUDA(cudaStreamSynchronize(d->cs));
+    }
+  }
+  LKV_CATCH
 }
 
 int lkv_device_read_host_slot(lkv_device* d, int64_t slot, void* dst) {

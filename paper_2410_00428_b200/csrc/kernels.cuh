@@ -46,12 +46,39 @@ struct TableUpdate {
   int pad;
 };
 
+// Device mirror of the two LIFO free lists (reference SlotPool,
+// kv_manager.cpp:52-74). A stack is [total-1 ... next_fresh] + pushed[0..size)
+// (kv_manager.hpp FreeListDelta); a sync writes the changed tail
+// pushed[low..size) and the header {total, next_fresh, size}. List 0 = GPU,
+// 1 = CPU.
+struct FreeSync {
+  const unsigned* src[2];  // uploaded pushed[low..size) of each list
+  unsigned* dst[2];        // device stacks
+  long long low[2], n[2], total[2], fresh[2], size[2];
+  long long* hdr;          // [2][3] = {total, next_fresh, pushed size} per list
+  int any;
+};
+
+// Applies a batch of block-table updates (last update per entry only, see
+// lkv_device::dedupe_journal) and, in the same launch, the free-list sync.
 __global__ void table_apply_kernel(const TableUpdate* __restrict__ upd, int n,
-                                   int* __restrict__ table) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+                                   int* __restrict__ table, FreeSync fs) {
+  const long long tid = blockIdx.x * (long long)blockDim.x + threadIdx.x, nt = (long long)gridDim.x * blockDim.x;
+  for (long long i = tid; i < n; i += nt) {
     const TableUpdate u = upd[i];
     table[u.index] = u.value;
   }
+  if (!fs.any) return;
+#pragma unroll
+  for (int l = 0; l < 2; ++l)
+    for (long long i = tid; i < fs.n[l]; i += nt) fs.dst[l][fs.low[l] + i] = fs.src[l][i];
+  if (tid == 0)
+#pragma unroll
+    for (int l = 0; l < 2; ++l) {
+      fs.hdr[3 * l] = fs.total[l];
+      fs.hdr[3 * l + 1] = fs.fresh[l];
+      fs.hdr[3 * l + 2] = fs.size[l];
+    }
 }
 
 // ---------------------------------------------------------------------------

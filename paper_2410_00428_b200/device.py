@@ -228,6 +228,16 @@ class Device:
         self._lib.call("lkv_device_read_host_slot", self.handle, slot, buf)
         return buf.raw
 
+    def free_stack(self, gpu: bool = True):
+        """The device (HBM) mirror of the manager's free list, in
+        KvManager.free_stack's form (bottom to top)."""
+        n = C.c_int64()
+        which = 0 if gpu else 1
+        self._lib.call("lkv_device_free_stack", self.handle, which, None, 0, C.byref(n))
+        out = (C.c_uint32 * max(1, n.value))()
+        self._lib.call("lkv_device_free_stack", self.handle, which, out, n.value, C.byref(n))
+        return list(out)[:n.value]
+
     def host_tier_stats(self) -> _abi.HostTierStats:
         s = _abi.HostTierStats()
         self._lib.call("lkv_device_host_tier_stats", self.handle, C.byref(s))

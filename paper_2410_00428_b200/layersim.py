@@ -358,6 +358,16 @@ class KvManager:
         self._lib.call("lkv_kv_dump_table", self.handle, buf, n.value + 1, C.byref(n))
         return buf.raw[:n.value].decode()
 
+    def free_stack(self, gpu: bool = True):
+        """The LIFO free list as the reference's SlotPool keeps it
+        (kv_manager.hpp:153-166): bottom to top, next allocation last."""
+        n = C.c_int64()
+        which = 0 if gpu else 1
+        self._lib.call("lkv_kv_free_stack", self.handle, which, None, 0, C.byref(n))
+        out = (C.c_uint32 * max(1, n.value))()
+        self._lib.call("lkv_kv_free_stack", self.handle, which, out, n.value, C.byref(n))
+        return list(out)[:n.value]
+
     def dump_hash(self) -> int:
         h = C.c_uint64()
         self._lib.call("lkv_kv_dump_hash", self.handle, C.byref(h))

@@ -70,15 +70,16 @@ def peaked_q(dev, layer, kv_lens, mode, seed=SEED, gen_seed=0):
     against a background of std ~5, so the running maximum jumps by ~11
     (~16 in log2, past kLazyMax = 8) at tiles and chunks deep in the
     sequence, and the output is dominated by the last anchor's V.
-    mode "extreme": weights 5, 15, 25, 35 — the anchors' scores rise by
-    ~165 in log2 over the sequence, past fp32's exponent range, so a kernel
-    that stopped re-basing its running maximum would overflow."""
+    mode "extreme": weights 5, 20, 40, 60 — the last anchor's score (~227)
+    stands ~160 (~230 in log2) above the background maximum of its tile's
+    predecessors, past fp32's exponent range, so a kernel that stopped
+    re-basing its running maximum would overflow."""
     import torch
     import oracle
     n = len(kv_lens)
     hq, hl, d = dev.q_heads_local, dev.kv_heads_local, dev.head_dim
     group = hq // hl
-    coef = (5.0, 15.0, 25.0, 35.0) if mode == "extreme" else (2.0, 5.0, 8.0, 11.0)
+    coef = (5.0, 20.0, 40.0, 60.0) if mode == "extreme" else (2.0, 5.0, 8.0, 11.0)
     if mode == "scaled":
         return (random_q(n, hq, d, 2000 + layer + gen_seed).float() * 16).to(torch.bfloat16)
     re = oracle.restatement()

@@ -48,16 +48,19 @@ class Rng:
 
 
 def fuzz_ops(lib, seed=31, rounds=10, steps=300, gpu=256, cpu=512, model=None, max_prompt=64,
-             check_every=1, record_tables=False):
+             check_every=1, record_tables=False, record_free=False, on_kv=None):
     """test_kv_manager.cpp:265-322 op mix, replayed through `lib`.
 
     Returns a list of per-op observations (all return values, free counts,
-    dump hash), one list per round."""
+    dump hash), one list per round. record_free: also the two LIFO free
+    stacks (kv_manager.hpp SlotPool). on_kv(kv) -> per-step callback or None
+    (e.g. binds a Device and checks its mirror after every op)."""
     model = model or ls.tiny8()
     rng = Rng(seed)
     out = []
     for _ in range(rounds):
         kv = ls.KvManager(ls.BlockPools(gpu, cpu, 16), model, lib=lib)
+        step_cb = on_kv(kv) if on_kv else None
         live, jobs, next_id = [], [], 0
         trace = []
         for step in range(steps):
@@ -98,8 +101,12 @@ def fuzz_ops(lib, seed=31, rounds=10, steps=300, gpu=256, cpu=512, model=None, m
                 obs += [f.gpu, f.cpu, f.deferred_gpu]
                 del live[pick]
             kv.check_conservation()
+            if step_cb:
+                step_cb(step)
             if step % check_every == 0:
                 obs += [kv.gpu_blocks_free(), kv.cpu_blocks_free(), format(kv.dump_hash(), "016x")]
+                if record_free:
+                    obs += [kv.free_stack(True), kv.free_stack(False)]
                 for rid in live[:3]:
                     obs += [kv.gpu_row_cost(rid), kv.cpu_row_cost(rid),
                             [(j.layer, j.bytes) for j in kv.plan_decode_fetch(rid)]]
@@ -108,7 +115,10 @@ def fuzz_ops(lib, seed=31, rounds=10, steps=300, gpu=256, cpu=512, model=None, m
             kv.complete_offload(j)
         for rid in live:
             kv.release(rid)
-        trace.append(["final", kv.gpu_blocks_free(), kv.cpu_blocks_free()])
+        if step_cb:
+            step_cb(-1)
+        trace.append(["final", kv.gpu_blocks_free(), kv.cpu_blocks_free()] +
+                     ([kv.free_stack(True), kv.free_stack(False)] if record_free else []))
         out.append(trace)
     return out
 

@@ -140,6 +140,24 @@ def test_attention_parity_peaked_softmax(mode, group, bs):
     dev.close()
 
 
+@pytest.mark.parametrize("mode", ["rising", "extreme"])
+@pytest.mark.parametrize("group", [2, 4, 8])
+def test_attention_parity_peaked_long_units(mode, group):
+    """As above, with enough KV (8 KV heads x 4 x 40k tokens) that the tcgen05
+    tile's chunking keeps 16-tile units (device.cu plan_chunks, the
+    production shape: config 3's batch uses them too). Anchors then land deep
+    inside a unit, so the in-tile lazy max raise and its O/l correction are
+    what keeps the result right, not the split merge."""
+    model = sc.gqa_model(L=2, hkv=8, group=group)
+    lens = [40000, 39000, 40960, 37777]
+    nb = sum((n + 15) // 16 for n in lens)
+    kv, dev = sc.make(model, gpu=nb * 2 + 64, cpu=nb * 2 + 64, max_blocks=2600, arena=nb + 64, max_batch=4)
+    for rid, n in enumerate(lens):
+        sc.prefill(kv, dev, rid, n, 1 if rid % 2 else 0)
+    sc.check_attention(dev, list(range(len(lens))), lens, layers=[1], q_mode=mode)
+    dev.close()
+
+
 @pytest.mark.parametrize("mode", [None, "rising"])
 def test_attention_parity_bench_shape_g1(mode):
     """The headline's shape: LLaMA-2-7B heads (Hkv = Hq = 32, G = 1, the
@@ -276,3 +294,35 @@ def test_table_journal_last_update_wins():
         kv.complete_offload(job.job_id)  # journal: every entry -> its CPU slot
         kv.release(0)                    # the row returns to the free list, same row next time
     dev.close()
+
+
+def test_free_list_mirror_after_rng31_fuzz():
+    """a4: the device's HBM mirror of both LIFO free lists (table_apply_kernel
+    applies the manager's free-list journal with the table journal) equals
+    the host stacks after every op of the Rng(31) stream of
+    test_kv_manager.cpp:265-322 — escalations, completions, orphaned
+    releases included — and the host stacks equal the reference SlotPool's
+    (tests/test_parity_bookkeeping.py::test_fuzz_free_stacks_vs_reference)."""
+    from paper_2410_00428_b200.device import Device, DeviceConfig
+    from tests import _drivers as drv
+    model = ls.ModelSpec(8, 4, 4, 128, 512, 1e8, 2)  # the fuzz's 8 layers, d_head 128 for the device
+    checked = []
+    devs = []
+
+    def bind(kv):
+        dev = Device(kv, model, 16, DeviceConfig(device=0, gpu_slots=256, host_slots=512, arena_slots=64,
+                                                 max_requests=160, max_blocks=40, max_batch=4, staging_chunks=4,
+                                                 chunk_bytes=1 << 20))
+        devs.append(dev)
+
+        def check(step):
+            if step % 7 and step != -1:
+                return
+            for gpu in (True, False):
+                assert dev.free_stack(gpu) == kv.free_stack(gpu), (step, gpu)
+            checked.append(step)
+        return check
+    drv.fuzz_ops(None, seed=31, rounds=3, steps=300, model=model, on_kv=bind)
+    for d in devs:
+        d.close()
+    assert len(checked) > 100 and checked.count(-1) == 3

@@ -75,6 +75,18 @@ def test_fuzz_live_vs_reference(prod, ref, seed):
     assert drv.fuzz_ops(prod, **kw) == drv.fuzz_ops(ref, **kw)
 
 
+@pytest.mark.parametrize("seed", [31, 2024])
+def test_fuzz_free_stacks_vs_reference(prod, ref, seed):
+    """The LIFO free lists themselves (reference SlotPool::free_stack_,
+    kv_manager.hpp:153-166, read from the compiled reference) after every
+    op of the test_kv_manager.cpp:265-322 stream: the product's compact
+    lazy stack must be the same stack, bottom to top."""
+    kw = dict(seed=seed, rounds=3, steps=300, gpu=96 if seed == 2024 else 256, cpu=64 if seed == 2024 else 512,
+              record_free=True)
+    a, b = drv.fuzz_ops(prod, **kw), drv.fuzz_ops(ref, **kw)
+    assert a == b, _first_diff(a[0], b[0])
+
+
 @pytest.mark.parametrize("seed", [3, 5])
 def test_fuzz_live_llama_shape(prod, ref, seed):
     """32-layer model, bigger prompts: exercises the tail-scan fetch path."""
