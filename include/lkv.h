@@ -370,11 +370,11 @@ typedef struct lkv_decode_stats {
   int64_t attn_launches;
   int64_t kernel_launches;       /* every kernel this iteration launched (snapshot, attention, merge) */
   double attn_ms;                /* summed CUDA-event time of the attention launches: the attention kernel
-                                    plus its PDL-overlapped split merge (LKV_SPLIT_TIMING=1: kernel alone) */
+                                    plus its PDL-overlapped split merge (one event interval per layer) */
   double h2d_ms;                 /* copy-engine busy time: summed CUDA-event time of each layer's prefetch copies */
   double iteration_ms;           /* decode_begin -> decode_end on the device */
   double h2d_span_ms;            /* first prefetch copy start -> last prefetch copy end */
-  double merge_ms;               /* split-merge time when LKV_SPLIT_TIMING=1, else 0 (inside attn_ms) */
+  double merge_ms;               /* always 0: the merge is timed inside attn_ms (kept for ABI stability) */
   double kernel_ms;              /* attention kernels alone: first CTA start -> last warp end on %globaltimer,
                                     summed over layers (no launch latency, no merge) */
 } lkv_decode_stats;

@@ -19,7 +19,7 @@
 //    the log2 domain; P.V in fp32. G query heads of a GQA group share every
 //    K/V byte.
 //  * Each unit writes an unnormalised partial (m, l, o), merged per
-//    (sequence, query head) by decode_merge_v4_kernel (one CTA each).
+//    (sequence, query head) by decode_merge_v5_kernel (one CTA each).
 #pragma once
 
 #include <cuda_bf16.h>
@@ -124,72 +124,6 @@ __device__ __forceinline__ void cvt8(const uint4& u, float* f) {
 constexpr int kSubTok = 16;                   // tokens per sub-tile
 constexpr int kHeadDim = 128;
 constexpr int kSubBytes = kSubTok * kHeadDim * 2;  // 4 KiB of K (or V) per head
-
-// Split merge of one (sequence, KV head): folds every chunk's unnormalised
-// partial into the output rows of the group's query heads,
-//   out[m][hq][d] = sum_c 2^(m_c - M) o_c / sum_c 2^(m_c - M) l_c.
-// NT cooperating threads, thread t owns dims [t*128/NT, (t+1)*128/NT), query
-// heads g0, g0+gstep, ...; lanes stride over chunks for the maxima and the
-// weights, and the o rows stream with 8 loads in flight per thread.
-// (Fusing this into the attention kernels' last unit was measured slower:
-// the per-unit fence + election cost more than the extra launch.)
-template <int NT>
-__device__ __forceinline__ void merge_kv_head(const float* __restrict__ part_o, const float* __restrict__ part_ml,
-                                              int chunk0, int nch, int h, int Hl, int G, long long out_row0,
-                                              void* __restrict__ out, int out_f32, int t, int g0 = 0,
-                                              int gstep = 1) {
-  constexpr int DPT = kHeadDim / NT;
-  const int lane = t & 31;
-  const long long cstride = static_cast<long long>(Hl) * G;  // partial units between chunks
-  for (int g = g0; g < G; g += gstep) {
-    const long long pu0 = (static_cast<long long>(chunk0) * Hl + h) * G + g;
-    // per-chunk maxima: lanes stride over the chunks (one round trip for <= 32)
-    float M = -INFINITY;
-    for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(part_ml + (pu0 + c * cstride) * 2));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float o[DPT], L = 0.f;
-#pragma unroll
-    for (int i = 0; i < DPT; ++i) o[i] = 0.f;
-    for (int c0 = 0; c0 < nch; c0 += 32) {
-      const int c = c0 + lane;
-      float f = 0.f;
-      if (c < nch) {
-        const float2 ml = __ldcg(reinterpret_cast<const float2*>(part_ml + (pu0 + c * cstride) * 2));
-        f = (ml.x == -INFINITY) ? 0.f : exp2f(ml.x - M);
-        L = fmaf(f, ml.y, L);
-      }
-      const int n = min(32, nch - c0);
-      // weighted sum of the chunks' o rows, 8 loads in flight per thread
-#pragma unroll 8
-      for (int k = 0; k < n; ++k) {
-        const float fk = __shfl_sync(0xffffffffu, f, k);
-        const float* src = part_o + (pu0 + (c0 + k) * cstride) * kHeadDim + t * DPT;
-        if constexpr (DPT == 4) {
-          const float4 v = __ldcg(reinterpret_cast<const float4*>(src));
-          o[0] = fmaf(fk, v.x, o[0]);
-          o[1] = fmaf(fk, v.y, o[1]);
-          o[2] = fmaf(fk, v.z, o[2]);
-          o[3] = fmaf(fk, v.w, o[3]);
-        } else {
-#pragma unroll
-          for (int i = 0; i < DPT; ++i) o[i] = fmaf(fk, __ldcg(src + i), o[i]);
-        }
-      }
-    }
-#pragma unroll
-    for (int o2 = 16; o2 > 0; o2 >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o2);
-    const float inv = L > 0.f ? 1.f / L : 0.f;
-    const long long idx = (out_row0 + g) * kHeadDim + t * DPT;
-#pragma unroll
-    for (int i = 0; i < DPT; ++i) {
-      if (out_f32)
-        static_cast<float*>(out)[idx + i] = o[i] * inv;
-      else
-        static_cast<__nv_bfloat16*>(out)[idx + i] = __float2bfloat16_rn(o[i] * inv);
-    }
-  }
-}
 
 template <int G, int BS, int W, int S>
 struct AttnV2 {
@@ -383,20 +317,6 @@ __global__ void __launch_bounds__(W * 32, 1) decode_attn_v2_kernel(
   stamp_end(stamps);
 }
 
-// One warp per (member, query head); 4 warps per CTA.
-__global__ void __launch_bounds__(128) decode_merge_v3_kernel(const float* __restrict__ part_o,
-                                                              const float* __restrict__ part_ml,
-                                                              const AttnSeq* __restrict__ seqs, int n, int Hl, int G,
-                                                              void* __restrict__ out, int out_f32) {
-  const int w = blockIdx.x * 4 + (threadIdx.x >> 5);
-  const int Hq = Hl * G;
-  if (w >= n * Hq) return;
-  const int m = w / Hq, hq = w % Hq, h = hq / G, g = hq % G;
-  const AttnSeq sd = seqs[m];
-  merge_kv_head<32>(part_o, part_ml, sd.chunk0, sd.nchunk, h, Hl, G, (static_cast<long long>(m) * Hl + h) * G, out,
-                    out_f32, threadIdx.x & 31, g, G);
-}
-
 // Fused all-gather of the per-head outputs (the path's one
 // exchange). Every rank's gather buffer (cudaMalloc'd by its lkv_device,
 // opened by the peers through CUDA IPC) is
@@ -576,139 +496,6 @@ __global__ void __launch_bounds__(W * 32) decode_merge_v5_kernel(const float* __
     }
   }
   merge_store_row(r, Lt, m, hq, Hl, G, out, out_f32, ga);
-}
-
-// One CTA (4 warps) per (member, query head). Every warp finds the global max
-// over the chunks (lanes stride over chunks), then warp w folds chunks w,
-// w+4, ... with all its o-row loads issued before any FMA (8 in flight per
-// lane), and the four partial sums meet in shared memory.
-__global__ void __launch_bounds__(128) decode_merge_v4_kernel(const float* __restrict__ part_o,
-                                                              const float* __restrict__ part_ml,
-                                                              const AttnSeq* __restrict__ seqs, int Hl, int G,
-                                                              void* __restrict__ out, int out_f32,
-                                                              GatherArgs ga) {
-  __shared__ float4 so[4][32];
-  __shared__ float sl[4];
-  const int m = blockIdx.x, hq = blockIdx.y, h = hq / G, g = hq % G;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const AttnSeq sd = seqs[m];
-  const int nch = sd.nchunk;
-  const long long cstride = static_cast<long long>(Hl) * G;
-  const long long pu0 = (static_cast<long long>(sd.chunk0) * Hl + h) * G + g;
-  float M = -INFINITY;
-  for (int c = lane; c < nch; c += 32) M = fmaxf(M, __ldcg(part_ml + (pu0 + c * cstride) * 2));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-  float L = 0.f;
-  if (M != -INFINITY) {
-    for (int c0 = warp; c0 < nch; c0 += 4 * 8) {
-      float4 v[8];
-      float2 ml[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // issue every load of the batch first
-        const int c = c0 + 4 * i;
-        if (c < nch) {
-          const long long pu = pu0 + c * cstride;
-          v[i] = __ldcg(reinterpret_cast<const float4*>(part_o + pu * kHeadDim) + lane);
-          ml[i] = __ldcg(reinterpret_cast<const float2*>(part_ml + pu * 2));
-        } else {
-          v[i] = make_float4(0.f, 0.f, 0.f, 0.f);
-          ml[i] = make_float2(-INFINITY, 0.f);
-        }
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float f = (ml[i].x == -INFINITY) ? 0.f : exp2f(ml[i].x - M);
-        L = fmaf(f, ml[i].y, L);
-        acc.x = fmaf(f, v[i].x, acc.x);
-        acc.y = fmaf(f, v[i].y, acc.y);
-        acc.z = fmaf(f, v[i].z, acc.z);
-        acc.w = fmaf(f, v[i].w, acc.w);
-      }
-    }
-  }
-  so[warp][lane] = acc;
-  if (lane == 0) sl[warp] = L;
-  __syncthreads();
-  if (warp == 0) {
-    float4 r = so[0][lane];
-#pragma unroll
-    for (int w = 1; w < 4; ++w) {
-      r.x += so[w][lane].x;
-      r.y += so[w][lane].y;
-      r.z += so[w][lane].z;
-      r.w += so[w][lane].w;
-    }
-    const float Lt = sl[0] + sl[1] + sl[2] + sl[3];
-    const float inv = Lt > 0.f ? 1.f / Lt : 0.f;
-    const long long idx = (static_cast<long long>(m) * Hl * G + hq) * kHeadDim + lane * 4;
-    if (out_f32) {
-      *reinterpret_cast<float4*>(static_cast<float*>(out) + idx) = make_float4(r.x * inv, r.y * inv, r.z * inv, r.w * inv);
-    } else {
-      __nv_bfloat16* o = static_cast<__nv_bfloat16*>(out) + idx;
-      o[0] = __float2bfloat16_rn(r.x * inv);
-      o[1] = __float2bfloat16_rn(r.y * inv);
-      o[2] = __float2bfloat16_rn(r.z * inv);
-      o[3] = __float2bfloat16_rn(r.w * inv);
-    }
-    if (ga.bases) {  // this row into every rank's gather buffer (NVLink stores to peers)
-      uint2 pk;
-      pk.x = (static_cast<unsigned>(__bfloat16_as_ushort(__float2bfloat16_rn(r.y * inv))) << 16) |
-             __bfloat16_as_ushort(__float2bfloat16_rn(r.x * inv));
-      pk.y = (static_cast<unsigned>(__bfloat16_as_ushort(__float2bfloat16_rn(r.w * inv))) << 16) |
-             __bfloat16_as_ushort(__float2bfloat16_rn(r.z * inv));
-      const long long row = (static_cast<long long>(ga.parity) * ga.max_batch + m) * ga.hq_total +
-                            static_cast<long long>(ga.rank) * Hl * G + hq;
-      const long long off = kGatherFlagWords * 4 + row * kHeadDim * 2 + lane * 8;
-      for (int p = 0; p < ga.n; ++p) *reinterpret_cast<uint2*>(ga.bases[p] + off) = pk;
-    }
-  }
-  if (ga.bases) {  // the launch's last CTA publishes the epoch to every rank
-    __threadfence_system();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      const unsigned total = gridDim.x * gridDim.y;
-      if (atomicAdd(ga.done, 1u) == total - 1) {
-        __threadfence_system();
-        for (int p = 0; p < ga.n; ++p)
-          st_release_sys(reinterpret_cast<unsigned*>(ga.bases[p]) + ga.rank, ga.epoch);
-        *ga.done = 0u;
-      }
-    }
-  }
-}
-
-// Previous merge (one CTA per (member, query head), thread = dim).
-// out[m][hq][d] over the member's chunks (unit = chunk * Hl + kv head).
-__global__ void decode_merge_v2_kernel(const float* __restrict__ part_o, const float* __restrict__ part_ml,
-                                       const AttnSeq* __restrict__ seqs, int Hl, int G, void* __restrict__ out,
-                                       int out_f32) {
-  const int m = blockIdx.x, hq = blockIdx.y, d = threadIdx.x;
-  const int h = hq / G, g = hq % G;
-  const AttnSeq sd = seqs[m];
-  float M = -INFINITY;
-  for (int j = 0; j < sd.nchunk; ++j) {
-    const long long pu = (static_cast<long long>(sd.chunk0 + j) * Hl + h) * G + g;
-    M = fmaxf(M, part_ml[pu * 2]);
-  }
-  float o = 0.f, L = 0.f;
-  if (M != -INFINITY) {
-    for (int j = 0; j < sd.nchunk; ++j) {
-      const long long pu = (static_cast<long long>(sd.chunk0 + j) * Hl + h) * G + g;
-      const float mc = part_ml[pu * 2];
-      if (mc == -INFINITY) continue;
-      const float f = exp2f(mc - M);
-      o += f * part_o[pu * kHeadDim + d];
-      L += f * part_ml[pu * 2 + 1];
-    }
-  }
-  const long long idx = (static_cast<long long>(m) * Hl * G + hq) * kHeadDim + d;
-  const float val = L > 0.f ? o / L : 0.f;
-  if (out_f32)
-    static_cast<float*>(out)[idx] = val;
-  else
-    static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(val);
 }
 
 }  // namespace lkv

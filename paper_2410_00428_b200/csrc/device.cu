@@ -25,7 +25,6 @@
 
 #include "decode_attn.cuh"
 #include "decode_gqa_tc.cuh"
-#include "prefill_attn.cuh"
 #include "prefill_attn2.cuh"
 #include "host_tier.hpp"
 #include "kernels.cuh"
@@ -167,10 +166,10 @@ struct lkv_device final : layersim::KvObserver {
   AttnChunk* d_chunks = nullptr;   // chunk list of the iteration (v2)
   long long chunk_cap = 0, part_cap = 0;
   int n_chunks = 0;
-  // 1 = split-K CUDA-core kernel, 2 = persistent CUDA-core kernel fed by TMA
-  // bulk copies (decode_attn.cuh), 3 = tcgen05 GQA tile (decode_gqa_tc.cuh).
-  // LKV_DECODE_KERNEL overrides the per-group-size default.
-  int kernel_version = 2;
+  // Decode attention kernel by GQA group size: G = 1 the persistent CUDA-core
+  // kernel fed by TMA bulk copies (decode_attn.cuh), G >= 2 the tcgen05 GQA
+  // tile (decode_gqa_tc.cuh).
+  bool tc_decode() const { return G >= 2; }
   // ---- fused all-gather of per-head outputs (decode_attn.cuh GatherArgs)
   char* d_gather = nullptr;                 // own gather buffer: flags | 2 parities of rows
   std::size_t gather_bytes = 0;
@@ -188,14 +187,10 @@ struct lkv_device final : layersim::KvObserver {
   std::size_t vh_cap = 0;
   cudaEvent_t vh_free = nullptr;
   bool vh_used = false;
-  bool pdl = true;                 // LKV_PDL=0: merge launched without programmatic dependent launch
-  // LKV_SPLIT_TIMING=1: an event between attention and merge, so attn_ms and
-  // merge_ms are separate. Off by default: with the host link saturated by the
-  // prefetch, that event alone adds ~20 us per layer and it defeats PDL, so
-  // attn_ms covers the attention + merge pair and merge_ms stays 0.
-  bool split_timing = false;
-  int merge_warps = 4;             // LKV_MERGE_WARPS=8: wider merge CTA (does not fit beside an attention CTA)
-  int merge_version = 5;           // LKV_MERGE=2 / 3 / 4: earlier merge kernels (thread = dim / warp per head / two-pass 4 warps)
+  // Timing mode records no event between attention and merge: with the host
+  // link saturated by the prefetch that event alone adds ~20 us per layer and
+  // defeats programmatic dependent launch, so attn_ms covers the attention +
+  // merge pair and merge_ms stays 0.
   CUtensorMap kvmap{};             // bf16 rows of 128 d over pool + arena frames, box {64, bs}
   float* d_part_o = nullptr;
   float* d_part_ml = nullptr;
@@ -309,18 +304,6 @@ struct lkv_device final : layersim::KvObserver {
     // G >= 2: the group's QK^T / PV are dense enough that CUDA cores fall
     // behind HBM (32k x 16, scripts/attn_micro.py: v2 85/70/39% of peak at
     // G=2/4/8) -> tcgen05 tile (95/93/89%).
-    kernel_version = G >= 2 ? 3 : 2;
-    if (const char* kv = std::getenv("LKV_DECODE_KERNEL")) {
-      const int v = std::atoi(kv);
-      kernel_version = (v == 1 || v == 3) ? v : 2;
-    }
-    if (const char* e = std::getenv("LKV_PDL")) pdl = std::atoi(e) != 0;
-    if (const char* e = std::getenv("LKV_MERGE_WARPS")) merge_warps = std::atoi(e) == 8 ? 8 : 4;
-    if (const char* e = std::getenv("LKV_SPLIT_TIMING")) split_timing = std::atoi(e) != 0;
-    if (const char* mv = std::getenv("LKV_MERGE")) {
-      const int v = std::atoi(mv);
-      merge_version = (v >= 2 && v <= 4) ? v : 5;
-    }
     {
       const unsigned long long rows = static_cast<unsigned long long>(std::max<long long>(frames, 1)) * 2 * Hl * bs;
       if (rows > 0x7FFFFFFFull) throw CapacityError("pool + arena rows exceed the TMA coordinate range");
@@ -661,15 +644,9 @@ struct lkv_device final : layersim::KvObserver {
   void scatter_blocks(const __nv_bfloat16* kb, const __nv_bfloat16* vb, long long tokens, long long b0, long long n,
                       const int* frames, char* dst) {
     if (n <= 0) return;
-    if (D == 128 && (bs & (bs - 1)) == 0) {
-      scatter_slots_kernel<<<static_cast<unsigned>(2 * n), 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b0), frames,
-                                                                        dst, sb, Hl, __builtin_ctz(bs));
-    } else {
-      const long long vecs = n * sb / 16;
-      const int grid = static_cast<int>(std::min<long long>((vecs + 255) / 256, 8ll * sms));
-      scatter_kv_kernel<<<grid, 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b0), static_cast<int>(n), frames, dst,
-                                              sb, Hl, bs, D);
-    }
+    // D = 128 and bs in {16, 32, 64} (init): one CTA per K or V half slot
+    scatter_slots_kernel<<<static_cast<unsigned>(2 * n), 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b0), frames,
+                                                                      dst, sb, Hl, __builtin_ctz(bs));
     LKV_CUDA(cudaGetLastError());
   }
 
@@ -955,7 +932,7 @@ struct lkv_device final : layersim::KvObserver {
     if (timing) LKV_CUDA(cudaEventRecord(t_it0, cs));
     LKV_CUDA(cudaMemcpyAsync(d_seqs, desc, std::max(n, 1) * sizeof(SeqDesc), cudaMemcpyHostToDevice, cs));
     ring.commit(cs);
-    if (kernel_version >= 2) plan_chunks();
+    plan_chunks();
     if (n > 0 && max_nblk > 0) {
       // one launch resolves every layer; layer l's arena stage is l % depth
       dim3 grid((max_nblk + 255) / 256, n, L);
@@ -964,13 +941,15 @@ struct lkv_device final : layersim::KvObserver {
                                                    cfg.arena_slots, cfg.pipeline_depth, d_snap);
       LKV_CUDA(cudaGetLastError());
     }
-    // Prefetches start after every D2H issued so far (the reference bus is
-    // serial: a layer's D2H precedes a later H2D of it).
-    cudaEvent_t ev;
-    ev_create(&ev);
-    LKV_CUDA(cudaEventRecord(ev, d2h));
-    LKV_CUDA(cudaStreamWaitEvent(h2d, ev, 0));
-    cudaEventDestroy(ev);
+    // A member's prefetch reads CPU frames its own prefill offload may still
+    // be writing: wait for that request's last prefill D2H only. Escalation
+    // jobs need no wait (their entries stay GPU-located until
+    // complete_offload, which synchronises the job's copies first), so the
+    // D2H and H2D engines keep running concurrently (full duplex).
+    for (const Member& m : members) {
+      auto pe = prefill_ev.find(m.id);
+      if (pe != prefill_ev.end()) LKV_CUDA(cudaStreamWaitEvent(h2d, pe->second, 0));
+    }
     if (timing) {
       if (!d_stamps) LKV_CUDA(cudaMalloc(&d_stamps, static_cast<std::size_t>(std::max(L, 1)) * 16));
       LKV_CUDA(cudaMemsetAsync(d_stamps, 0, static_cast<std::size_t>(std::max(L, 1)) * 16, cs));
@@ -985,20 +964,17 @@ struct lkv_device final : layersim::KvObserver {
   // The tensor-core kernel deals units to CTAs instead of warps and works in
   // 128-token tiles: chunks of up to 16 tiles, never below one tile.
   void plan_chunks() {
-    const bool tc_path = kernel_version == 3;
-    const long long workers = static_cast<long long>(sms) * (tc_path ? 1 : v2_warps(G));
+    const bool tc_path = tc_decode();
+    const long long workers = static_cast<long long>(sms) * (tc_path ? 1 : 12);
     const long long block_heads = static_cast<long long>(total_blocks) * Hl;
     const int tile_blocks = 128 / bs;
     int cb = tc_path ? 16 * tile_blocks : 32;
     const int cb_min = tc_path ? tile_blocks : 1;
     // units per worker before halving the chunk: the tensor-core kernel's
     // per-unit epilogue favours fewer, longer units (measured: 4 -> 85%, 8 ->
-    // 81% on the 70B TP8 shard; flat on 8B), the CUDA-core one balances at 8.
-    static const long long env_per_worker = [] {
-      const char* e = std::getenv("LKV_UNITS_PER_WORKER");
-      return e ? std::max(1ll, std::atoll(e)) : 0ll;
-    }();
-    const long long per_worker = env_per_worker ? env_per_worker : (tc_path ? 4 : 8);
+    // 81% on the 70B TP8 shard; flat on 8B), the CUDA-core one balances at 8
+    // (profiles/r1y_decode_micro.jsonl).
+    const long long per_worker = tc_path ? 4 : 8;
     while (cb > cb_min && block_heads / cb < per_worker * workers) cb >>= 1;
     std::vector<AttnChunk> ch;
     auto* aseq = reinterpret_cast<AttnSeq*>(ring.reserve(std::max<std::size_t>(members.size(), 1) * sizeof(AttnSeq)));
@@ -1034,11 +1010,6 @@ struct lkv_device final : layersim::KvObserver {
     }
   }
 
-  // Warps x stages per CTA (one CTA per SM). Measured on B200 (scripts/
-  // attn_micro.py, 7 x 16k, 7B): G=1 12x2 91% of HBM peak, 8x3 89%, 6x4 91%.
-  // G>=2 keeps 8x3 (register-limited to 8 warps).
-  static int v2_warps(int g) { return g == 1 ? 12 : 8; }
-
   // Opt-in dynamic shared memory, once per kernel on this device (the
   // attribute is per device context, so it is tracked per lkv_device).
   std::unordered_set<const void*> smem_attr_done;
@@ -1050,7 +1021,7 @@ struct lkv_device final : layersim::KvObserver {
 
   // ---- v3: tcgen05 GQA tile (decode_gqa_tc.cuh) -------------------------------
   template <int GG, int BB>
-  void launch_tc(int l, const void* q, float sl2, void* out, int f32) {
+  void launch_tc(int l, const void* q, float sl2) {
     constexpr int NS = 3;
     using K = GqaTc<GG, BB, NS>;
     auto fn = decode_gqa_tc_kernel<GG, BB, NS>;
@@ -1063,53 +1034,25 @@ struct lkv_device final : layersim::KvObserver {
   }
 
   template <int GG>
-  void launch_tc_bs(int l, const void* q, float sl2, void* out, int f32) {
-    if (bs == 16) launch_tc<GG, 16>(l, q, sl2, out, f32);
-    else if (bs == 32) launch_tc<GG, 32>(l, q, sl2, out, f32);
-    else launch_tc<GG, 64>(l, q, sl2, out, f32);
+  void launch_tc_bs(int l, const void* q, float sl2) {
+    if (bs == 16) launch_tc<GG, 16>(l, q, sl2);
+    else if (bs == 32) launch_tc<GG, 32>(l, q, sl2);
+    else launch_tc<GG, 64>(l, q, sl2);
   }
 
-  template <int GG, int BB, int W, int S>
-  void launch_v2_cfg(int l, const void* q, float sl2, void* out, int f32) {
-    using K = AttnV2<GG, BB, W, S>;
-    auto fn = decode_attn_v2_kernel<GG, BB, W, S>;
+  // G = 1: 12 warps x 2 stages per CTA (scripts/attn_micro.py, 7 x 16k, 7B:
+  // 12x2 91% of HBM peak, 8x3 89%, 6x4 91%).
+  template <int BB>
+  void launch_v2(int l, const void* q, float sl2) {
+    constexpr int W = 12, S = 2;
+    using K = AttnV2<1, BB, W, S>;
+    auto fn = decode_attn_v2_kernel<1, BB, W, S>;
     smem_attr(reinterpret_cast<const void*>(fn), K::kSmem);
     const int units = n_chunks * Hl;
     const int grid = std::max(1, std::min(sms, (units + W - 1) / W));
     fn<<<grid, K::kThreads, K::kSmem, cs>>>(dbuf, sb, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots,
                                             d_aseqs, d_chunks, units, static_cast<const __nv_bfloat16*>(q),
                                             d_part_o, d_part_ml, sl2, layer_stamps(l));
-  }
-
-  template <int GG, int BB>
-  void launch_v2(int l, const void* q, float sl2, void* out, int f32) {
-    if constexpr (GG == 1)
-      launch_v2_cfg<GG, BB, 12, 2>(l, q, sl2, out, f32);
-    else
-      launch_v2_cfg<GG, BB, 8, 3>(l, q, sl2, out, f32);
-  }
-
-  template <int GG>
-  void launch_v2_bs(int l, const void* q, float sl2, void* out, int f32) {
-    if (bs == 16) launch_v2<GG, 16>(l, q, sl2, out, f32);
-    else if (bs == 32) launch_v2<GG, 32>(l, q, sl2, out, f32);
-    else launch_v2<GG, 64>(l, q, sl2, out, f32);
-  }
-
-  template <int GG, int BB>
-  void launch_attn(int l, int n_split, int bps, const void* q, void* out, int f32, float scale_log2) {
-    dim3 grid(n_split, Hl, static_cast<unsigned>(members.size()));
-    decode_attn_kernel<GG, BB><<<grid, 128, 0, cs>>>(
-        dbuf, sb, Hl, d_snap + static_cast<long long>(l) * cfg.arena_slots, d_seqs,
-        static_cast<const __nv_bfloat16*>(q), out, f32, d_part_o,
-        d_part_ml, n_split, bps, scale_log2);
-  }
-
-  template <int GG>
-  void launch_attn_bs(int l, int n_split, int bps, const void* q, void* out, int f32, float sl2) {
-    if (bs == 16) launch_attn<GG, 16>(l, n_split, bps, q, out, f32, sl2);
-    else if (bs == 32) launch_attn<GG, 32>(l, n_split, bps, q, out, f32, sl2);
-    else launch_attn<GG, 64>(l, n_split, bps, q, out, f32, sl2);
   }
 
   // f2: write each member's new token (position fetch_len) of layer l wherever
@@ -1222,20 +1165,20 @@ struct lkv_device final : layersim::KvObserver {
     layer_epoch.assign(L, 0);
   }
 
-  // Merge v5 launched as a programmatic dependent of the attention kernel
-  // (LKV_PDL=0 turns it into a plain stream-ordered launch).
+  // Merge v5 (4 warps: fits beside a persistent attention CTA) launched as a
+  // programmatic dependent of the attention kernel.
   void launch_merge_v5(int n, void* out, int f32, GatherArgs ga) {
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(n, Hql);
-    lc.blockDim = dim3(merge_warps * 32);
+    lc.blockDim = dim3(4 * 32);
     lc.dynamicSmemBytes = 0;
     lc.stream = cs;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     at[0].val.programmaticStreamSerializationAllowed = 1;
     lc.attrs = at;
-    lc.numAttrs = pdl ? 1 : 0;
-    LKV_CUDA(cudaLaunchKernelEx(&lc, merge_warps == 8 ? decode_merge_v5_kernel<8> : decode_merge_v5_kernel<4>, static_cast<const float*>(d_part_o),
+    lc.numAttrs = 1;
+    LKV_CUDA(cudaLaunchKernelEx(&lc, decode_merge_v5_kernel<4>, static_cast<const float*>(d_part_o),
                                 static_cast<const float*>(d_part_ml), static_cast<const AttnSeq*>(d_aseqs), Hl, G,
                                 out, f32, ga));
   }
@@ -1251,71 +1194,27 @@ struct lkv_device final : layersim::KvObserver {
     const int n = static_cast<int>(members.size());
     if (timing) {
       LKV_CUDA(cudaEventRecord(t_attn0[l], cs));
-      LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // re-recorded after the attention kernel when one runs
     }
-    if (n > 0 && kernel_version >= 2) {
+    if (n > 0) {
       const float sl2 = scale * 1.4426950408889634f;
-      if (n_chunks > 0 && kernel_version == 3) {
+      if (n_chunks > 0) {
         switch (G) {
-          case 1: launch_tc_bs<1>(l, q, sl2, out, f32); break;
-          case 2: launch_tc_bs<2>(l, q, sl2, out, f32); break;
-          case 4: launch_tc_bs<4>(l, q, sl2, out, f32); break;
-          default: launch_tc_bs<8>(l, q, sl2, out, f32); break;
-        }
-        LKV_CUDA(cudaGetLastError());
-      } else if (n_chunks > 0) {
-        switch (G) {
-          case 1: launch_v2_bs<1>(l, q, sl2, out, f32); break;
-          case 2: launch_v2_bs<2>(l, q, sl2, out, f32); break;
-          case 4: launch_v2_bs<4>(l, q, sl2, out, f32); break;
-          default: launch_v2_bs<8>(l, q, sl2, out, f32); break;
+          case 1:
+            if (bs == 16) launch_v2<16>(l, q, sl2);
+            else if (bs == 32) launch_v2<32>(l, q, sl2);
+            else launch_v2<64>(l, q, sl2);
+            break;
+          case 2: launch_tc_bs<2>(l, q, sl2); break;
+          case 4: launch_tc_bs<4>(l, q, sl2); break;
+          default: launch_tc_bs<8>(l, q, sl2); break;
         }
         LKV_CUDA(cudaGetLastError());
       }
-      // attention kernel | merge kernel (an event between them costs the PDL overlap: LKV_SPLIT_TIMING=0 drops it)
-      if (timing && split_timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));
       // merge (members without KV get zero rows: no chunks, L = 0)
-      if (gather_on() && merge_version < 4) throw std::invalid_argument("fused gather needs merge v4/v5");
-      if (merge_version == 2)
-        decode_merge_v2_kernel<<<dim3(n, Hql), D, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32);
-      else if (merge_version == 3)
-        decode_merge_v3_kernel<<<(n * Hql + 3) / 4, 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, n, Hl, G, out, f32);
-      else if (merge_version == 4)
-        decode_merge_v4_kernel<<<dim3(n, Hql), 128, 0, cs>>>(d_part_o, d_part_ml, d_aseqs, Hl, G, out, f32,
-                                                             gather_args(l));
-      else
-        launch_merge_v5(n, out, f32, gather_args(l));
+      launch_merge_v5(n, out, f32, gather_args(l));
       LKV_CUDA(cudaGetLastError());
       dstats.attn_launches += 1;
       dstats.kernel_launches += n_chunks > 0 ? 2 : 1;
-    } else if (n > 0) {
-      if (gather_on()) throw std::invalid_argument("fused gather needs decode kernel v2/v3");
-      const int pairs = n * Hl;
-      const int target = 4 * sms;
-      int n_split = std::max(1, std::min((target + pairs - 1) / pairs, std::max(max_nblk, 1)));
-      int bps = (std::max(max_nblk, 1) + n_split - 1) / n_split;
-      bps = std::min(bps, 256);
-      n_split = (std::max(max_nblk, 1) + bps - 1) / bps;
-      if (n_split > kMaxSplits) {
-        n_split = kMaxSplits;
-        bps = (max_nblk + n_split - 1) / n_split;
-        if (bps > 256) throw CapacityError("decode: context too long for split table");
-      }
-      const float sl2 = scale * 1.4426950408889634f;
-      switch (G) {
-        case 1: launch_attn_bs<1>(l, n_split, bps, q, out, f32, sl2); break;
-        case 2: launch_attn_bs<2>(l, n_split, bps, q, out, f32, sl2); break;
-        case 4: launch_attn_bs<4>(l, n_split, bps, q, out, f32, sl2); break;
-        default: launch_attn_bs<8>(l, n_split, bps, q, out, f32, sl2); break;
-      }
-      LKV_CUDA(cudaGetLastError());
-      if (timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));
-      dstats.attn_launches += 1;
-      dstats.kernel_launches += n_split > 1 ? 2 : 1;
-      if (n_split > 1) {
-        decode_merge_kernel<<<n * Hql, D, 0, cs>>>(d_part_o, d_part_ml, n_split, D, out, f32);
-        LKV_CUDA(cudaGetLastError());
-      }
     }
     if (n == 0 && gather_on()) {  // nothing to send, but peers still wait for this epoch
       const GatherArgs ga = gather_args(l);
@@ -1323,7 +1222,7 @@ struct lkv_device final : layersim::KvObserver {
       LKV_CUDA(cudaGetLastError());
     }
     if (timing) {
-      if (!split_timing) LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attn_ms = the pair
+      LKV_CUDA(cudaEventRecord(t_attnk[l], cs));  // attn_ms = the attention + merge pair
       LKV_CUDA(cudaEventRecord(t_attn1[l], cs));
     }
     LKV_CUDA(cudaEventRecord(attn_done[st], cs));
@@ -1446,90 +1345,52 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   if (tokens > 0x7FFFFF80ll) throw std::invalid_argument("prefill_attention: too many tokens");
   cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : d->cs;
   const uint64_t T = static_cast<uint64_t>(tokens), D = static_cast<uint64_t>(d->D);
-  // LKV_PREFILL_P=bf16x2: P as bf16 hi + lo against bf16 V (two PV MMAs);
-  // default fp16 P against an fp16 copy of V (one PV MMA).
-  const char* ep = std::getenv("LKV_PREFILL_P");
-  const bool pf16 = !(ep && std::strcmp(ep, "bf16x2") == 0);
-  const void* vsrc = v;
-  if (pf16) {  // fp16 copy of V in a device scratch (bf16 -> fp16 is exact in fp16's normal range)
-    const std::size_t need = static_cast<std::size_t>(T) * d->Hl * D * 2;
-    if (need > d->vh_cap) {
-      LKV_CUDA(cudaDeviceSynchronize());
-      cudaFree(d->d_vh);
-      LKV_CUDA(cudaMalloc(&d->d_vh, need));
-      d->vh_cap = need;
-    }
-    if (d->vh_used) LKV_CUDA(cudaStreamWaitEvent(s, d->vh_free, 0));  // previous user of the scratch
-    const long long n8 = static_cast<long long>(need / 16);
-    const int grid = static_cast<int>(std::min<long long>((n8 + 255) / 256, 8ll * d->sms));
-    bf16_to_f16_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(v), static_cast<uint4*>(d->d_vh), n8);
-    LKV_CUDA(cudaGetLastError());
-    vsrc = d->d_vh;
+  // fp16 copy of V in a device scratch (bf16 -> fp16 is exact in fp16's
+  // normal range, saturating beyond it: the input contract in lkv.h)
+  const std::size_t need = static_cast<std::size_t>(T) * d->Hl * D * 2;
+  if (need > d->vh_cap) {
+    LKV_CUDA(cudaDeviceSynchronize());
+    cudaFree(d->d_vh);
+    LKV_CUDA(cudaMalloc(&d->d_vh, need));
+    d->vh_cap = need;
   }
+  if (d->vh_used) LKV_CUDA(cudaStreamWaitEvent(s, d->vh_free, 0));  // previous user of the scratch
+  const long long n8 = static_cast<long long>(need / 16);
+  const int grid = static_cast<int>(std::min<long long>((n8 + 255) / 256, 8ll * d->sms));
+  bf16_to_f16_kernel<<<grid, 256, 0, s>>>(static_cast<const uint4*>(v), static_cast<uint4*>(d->d_vh), n8);
+  LKV_CUDA(cudaGetLastError());
   CUtensorMap qm, km, vm;
   if (!tc::make_map_3d(&qm, q, D, d->Hql, T, D * 2, D * 2 * d->Hql, 64, 1, 128, true) ||
       !tc::make_map_3d(&km, k, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true) ||
-      !tc::make_map_3d(&vm, vsrc, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true,
-                       pf16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16))
+      !tc::make_map_3d(&vm, d->d_vh, D, d->Hl, T, D * 2, D * 2 * d->Hl, 64, 1, 128, true,
+                       CU_TENSOR_MAP_DATA_TYPE_FLOAT16))
     throw CudaError("prefill_attention: cuTensorMapEncodeTiled failed (pointers must be 16 B aligned)");
-  // LKV_PREFILL_WG=1: one softmax warpgroup per CTA (thread = whole row); default 2 (row split in halves)
-  static const int nwg = [] {
-    const char* e = std::getenv("LKV_PREFILL_WG");
-    return (e && std::atoi(e) == 1) ? 1 : 2;
-  }();
-  // LKV_PREFILL_KERNEL=1: the one-tile kernel (row halves); default with fp16
-  // P: two query tiles per CTA, one softmax warpgroup each (prefill_attn2.cuh).
-  const char* ek = std::getenv("LKV_PREFILL_KERNEL");
-  const int kver = ek ? std::atoi(ek) : 2;
-  const bool two_tile = kver != 1;
   const int nq_all = static_cast<int>((tokens + 127) / 128);
   // KV heads per dispatch chunk: as many as keep their K+V (T x 512 B per
-  // KV head, bf16 K + fp16 V) within 16 MB (LKV_PREFILL_L2_MB; measured
-  // best of 0 / 16 / 48 / 96 / all, profiles/r1ab_prefill_order.jsonl).
-  // LKV_PREFILL_L2_MB=0: one query head per chunk (pairs fastest).
-  static const long long l2_budget = [] {
-    const char* e = std::getenv("LKV_PREFILL_L2_MB");
-    return (e ? std::max(0ll, std::atoll(e)) : 16ll) << 20;
-  }();
+  // KV head, bf16 K + fp16 V) within 16 MB of L2 (measured best of
+  // 0 / 16 / 48 / 96 MB / all heads, profiles/r1ab_prefill_order.jsonl).
+  constexpr long long kL2Budget = 16ll << 20;
   const long long kv_per_head = static_cast<long long>(tokens) * 512;
-  const int chunk_kv = static_cast<int>(std::clamp<long long>(l2_budget / std::max(kv_per_head, 1ll), 1, d->Hl));
-  const int chunk_q = l2_budget == 0 ? 1 : chunk_kv * d->G;
+  const int chunk_kv = static_cast<int>(std::clamp<long long>(kL2Budget / std::max(kv_per_head, 1ll), 1, d->Hl));
+  const int chunk_q = chunk_kv * d->G;
   const long long npairs_all = (nq_all + 1) / 2;
-  if (pf16 && two_tile) {
-    // LKV_PREFILL_POLY = 0 / 25 / 50: share of exponentials computed on the FMA pipe
-    const char* epo = std::getenv("LKV_PREFILL_POLY");
-    const int poly = epo ? std::atoi(epo) : 0;
-    auto fn2 = poly >= 50 ? prefill_attn2_kernel<2> : poly >= 25 ? prefill_attn2_kernel<1> : prefill_attn2_kernel<0>;
-    d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
-    cudaLaunchConfig_t lc{};
-    lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));
-    lc.blockDim = dim3(320);
-    lc.dynamicSmemBytes = PrefillAttn2Smem::kBytes;
-    lc.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
-    lc.attrs = at;
-    lc.numAttrs = d->pdl ? 1 : 0;  // dependent of bf16_to_f16_kernel (LKV_PDL=0: plain launch)
-    LKV_CUDA(cudaLaunchKernelEx(&lc, fn2, qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0,
-                                static_cast<int>(tokens), d->Hql, d->G, scale * 1.4426950408889634f, chunk_q));
-    LKV_CUDA(cudaGetLastError());
-    LKV_CUDA(cudaEventRecord(d->vh_free, s));
-    d->vh_used = true;
-    return LKV_OK;
-  }
-  auto fn = nwg == 1 ? (pf16 ? prefill_attn_kernel<1, true> : prefill_attn_kernel<1, false>)
-                     : (pf16 ? prefill_attn_kernel<2, true> : prefill_attn_kernel<2, false>);
-  d->smem_attr(reinterpret_cast<const void*>(fn), PrefillAttnSmem::kBytes);
-  const dim3 grid(static_cast<unsigned>((tokens + 127) / 128), static_cast<unsigned>(d->Hql));
-  fn<<<grid, 96 + 128 * nwg, PrefillAttnSmem::kBytes, s>>>(
-      qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0, static_cast<int>(tokens), d->Hql, d->G,
-      scale * 1.4426950408889634f);
+  auto fn2 = prefill_attn2_kernel<0>;
+  d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));
+  lc.blockDim = dim3(320);
+  lc.dynamicSmemBytes = PrefillAttn2Smem::kBytes;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;  // dependent of bf16_to_f16_kernel
+  lc.attrs = at;
+  lc.numAttrs = 1;
+  LKV_CUDA(cudaLaunchKernelEx(&lc, fn2, qm, km, vm, out, out_dtype == LKV_DTYPE_F32 ? 1 : 0,
+                              static_cast<int>(tokens), d->Hql, d->G, scale * 1.4426950408889634f, chunk_q));
   LKV_CUDA(cudaGetLastError());
-  if (pf16) {
-    LKV_CUDA(cudaEventRecord(d->vh_free, s));
-    d->vh_used = true;
-  }
+  LKV_CUDA(cudaEventRecord(d->vh_free, s));
+  d->vh_used = true;
   LKV_CATCH
 }
 

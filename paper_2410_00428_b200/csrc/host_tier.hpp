@@ -60,9 +60,8 @@ class HostTier {
     if (p == MAP_FAILED) throw std::runtime_error("host tier: mmap of the pageable homes failed");
     home_ = static_cast<char*>(p);
     // 2 MiB pages where the kernel allows them (THP "madvise" or "always"):
-    // a 256 KiB frame copy touches 64 base pages otherwise. LKV_TIER_THP=0 skips.
-    if (const char* e = std::getenv("LKV_TIER_THP"); !(e && e[0] == '0'))
-      madvise(home_, static_cast<std::size_t>(S_ * sb_), MADV_HUGEPAGE);
+    // a 256 KiB frame copy touches 64 base pages otherwise.
+    madvise(home_, static_cast<std::size_t>(S_ * sb_), MADV_HUGEPAGE);
     cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&pinned_), static_cast<std::size_t>(F_ * sb_),
                                   cudaHostAllocMapped | cudaHostAllocPortable);
     if (e != cudaSuccess) throw std::runtime_error(std::string("host tier: cudaHostAlloc: ") + cudaGetErrorString(e));
@@ -343,10 +342,9 @@ class HostTier {
     _mm_sfence();
   }
 
-  void copy_frame(char* dst, const char* src, std::size_t n) const {
-    if (nt_) stream_copy(dst, src, n);
-    else std::memcpy(dst, src, n);
-  }
+  // Non-temporal stores: frames are not re-read by this CPU, so they skip
+  // the cache (profiles/r1y_tier_nt_micro.jsonl).
+  void copy_frame(char* dst, const char* src, std::size_t n) const { stream_copy(dst, src, n); }
 
   template <class Fn>
   void copy_parallel(std::size_t n, Fn&& fn) {
@@ -380,10 +378,6 @@ class HostTier {
   std::thread cleaner_;
   bool stop_ = false;
   int threads_ = 8;
-  bool nt_ = [] {  // LKV_TIER_NT=0: plain memcpy
-    const char* e = std::getenv("LKV_TIER_NT");
-    return !(e && e[0] == '0');
-  }();
   HostTierStats st_;
 };
 

@@ -86,45 +86,11 @@ __global__ void table_apply_kernel(const TableUpdate* __restrict__ upd, int n,
 // Block b (tokens [b*bs, b*bs+bs)) goes to dst + frame[b] * slot_bytes, where
 // frame = the GPU slot ids from the table mirror (retained layer, scatter)
 // or b - b0 (offloaded layer, pack into a staging segment). Tokens past
-// `tokens` in the tail block are zero-filled. One 16 B vector per thread
-// step; consecutive threads write consecutive 16 B of a slot.
-__global__ void scatter_kv_kernel(const __nv_bfloat16* __restrict__ k,
-                                  const __nv_bfloat16* __restrict__ v, long long tokens,
-                                  int b0, int nblk, const int* __restrict__ frames,
-                                  char* __restrict__ dst, long long slot_bytes, int Hl, int bs,
-                                  int D) {
-  const int vec_per_row = D / 8;                        // 16 B vectors per (token, head)
-  const long long vec_per_slot = 2ll * Hl * bs * vec_per_row;
-  const long long total = vec_per_slot * nblk;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int bl = static_cast<int>(i / vec_per_slot);
-    long long r = i - bl * vec_per_slot;
-    const int c = static_cast<int>(r % vec_per_row);
-    r /= vec_per_row;
-    const int t = static_cast<int>(r % bs);
-    r /= bs;
-    const int h = static_cast<int>(r % Hl);
-    const int kvsel = static_cast<int>(r / Hl);
-    const int b = b0 + bl;
-    const long long tok = static_cast<long long>(b) * bs + t;
-    uint4 val = make_uint4(0, 0, 0, 0);
-    if (tok < tokens) {
-      const __nv_bfloat16* src = (kvsel == 0 ? k : v) + (tok * Hl + h) * D + c * 8;
-      val = ld_stream(src);
-    }
-    const long long frame = frames ? frames[b] : bl;
-    char* out = dst + frame * slot_bytes +
-                ((static_cast<long long>(kvsel) * Hl + h) * bs + t) * (D * 2) + c * 16;
-    st_stream(out, val);
-  }
-}
-
+// `tokens` in the tail block are zero-filled.
 // One CTA per half slot (K or V of block b0 + i): [Hl][bs][128] bf16, written
 // contiguously; source rows (token, head) of the prefill K/V. 32-bit index
 // math (bs = 1 << bs_shift, D = 128) and 4 independent 16 B loads in flight
-// per thread. Replaces the grid-stride scatter_kv_kernel on the hot path
-// (which spent its issue slots on 64-bit div/mod).
+// per thread.
 __global__ void __launch_bounds__(256) scatter_slots_kernel(const __nv_bfloat16* __restrict__ k,
                                                             const __nv_bfloat16* __restrict__ v, long long tokens,
                                                             int b0, const int* __restrict__ frames,
@@ -183,36 +149,6 @@ __global__ void __launch_bounds__(256) gather_slots_v2_kernel(const char* __rest
 }
 
 // ---------------------------------------------------------------------------
-// Gather: whole slots (list) -> contiguous staging, in list order (grid-stride
-// form, kept for reference; the path launches gather_slots_v2_kernel).
-__global__ void gather_slots_kernel(const char* __restrict__ pool, const unsigned* __restrict__ slots,
-                                    int n, long long slot_bytes, char* __restrict__ dst) {
-  const long long vec_per_slot = slot_bytes / 16;
-  const long long total = vec_per_slot * n;
-  const long long stride = (long long)gridDim.x * blockDim.x;
-  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  // 4 independent 16 B loads in flight per thread per iteration.
-  for (; i + 3 * stride < total; i += 4 * stride) {
-    uint4 v[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const long long j = i + u * stride;
-      const long long s = j / vec_per_slot;
-      v[u] = ld_stream(pool + static_cast<long long>(slots[s]) * slot_bytes +
-                       (j - s * vec_per_slot) * 16);
-    }
-#pragma unroll
-    for (int u = 0; u < 4; ++u) st_stream(dst + (i + u * stride) * 16, v[u]);
-  }
-  for (; i < total; i += stride) {
-    const long long s = i / vec_per_slot;
-    st_stream(dst + i * 16,
-              ld_stream(pool + static_cast<long long>(slots[s]) * slot_bytes +
-                        (i - s * vec_per_slot) * 16));
-  }
-}
-
-// ---------------------------------------------------------------------------
 // Decode snapshot: resolve each (member, block) of one layer's table row into
 // a physical frame of the unified [pool | arena] buffer. GPU entries keep
 // their slot id; CPU entries (encoded ~cpu_slot) point at the arena frame the
@@ -265,231 +201,6 @@ __global__ void decode_snapshot_kernel(const int* __restrict__ table, const SeqD
     snap[sd.blk_offset + b] =
         e >= 0 ? e : static_cast<int>(arena0 + sd.blk_offset + b);
   }
-}
-
-// ---------------------------------------------------------------------------
-// Paged decode attention, split-K over blocks (flash-decoding style), GQA
-// group of G query heads per KV head handled by one CTA so each K/V byte is
-// read once. HBM-bound: per (seq, kv head) it streams kv_len*D*2*2 bytes.
-//
-// Work unit = a 16-token sub-tile of one block for one kv head: 4 KiB of K +
-// 4 KiB of V, loaded by one warp with 16 B vectors (lane: 16 B chunk c = dims
-// [8c, 8c+8) of rows r0 + 2k). Q.K partials are reduced across the 16 lanes
-// of a row pair with a value-splitting butterfly (8 shuffles for 8 rows).
-// Online softmax in the log2 domain; P.V accumulates fp32 per lane.
-template <int G, int BS>
-struct DecodeCfg {
-  static constexpr int kD = 128;
-  static constexpr int kWarps = 4;
-  static constexpr int kThreads = kWarps * 32;
-  static constexpr int kSubPerBlock = BS / 16;
-};
-
-// Attention output: bf16 (serving) or fp32 (parity checks at 1e-3 relative).
-__device__ __forceinline__ void store_out(void* out, int f32, long long i, float v) {
-  if (f32)
-    static_cast<float*>(out)[i] = v;
-  else
-    static_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
-}
-
-__device__ __forceinline__ void bf16x8_to_f32(const uint4& u, float* f) {
-  const unsigned w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    f[2 * i] = __uint_as_float(w[i] << 16);
-    f[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
-  }
-}
-
-template <int G, int BS>
-__global__ void __launch_bounds__(128) decode_attn_kernel(
-    const char* __restrict__ base, long long slot_bytes, int Hl,
-    const int* __restrict__ snap, const SeqDesc* __restrict__ seqs,
-    const __nv_bfloat16* __restrict__ q, void* __restrict__ out, int out_f32,
-    float* __restrict__ part_o, float* __restrict__ part_ml, int n_split, int blocks_per_split,
-    float scale_log2) {
-  using C = DecodeCfg<G, BS>;
-  constexpr int D = C::kD;
-  const int split = blockIdx.x, h = blockIdx.y, m = blockIdx.z;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = lane & 15, r0 = lane >> 4;
-  const int Hq = Hl * G;
-
-  __shared__ int s_tbl[256];
-  __shared__ float s_acc[C::kWarps][G][D];
-  __shared__ float s_m[C::kWarps][G], s_l[C::kWarps][G];
-
-  const SeqDesc sd = seqs[m];
-  const int jb0 = split * blocks_per_split;
-  const int jb1 = min(sd.n_blocks, jb0 + blocks_per_split);
-  const int nblk = max(0, jb1 - jb0);
-  for (int i = threadIdx.x; i < nblk; i += C::kThreads) s_tbl[i] = snap[sd.blk_offset + jb0 + i];
-
-  // q fragment: dims [8c, 8c+8) of each of the G heads, pre-scaled by
-  // softmax_scale * log2(e).
-  float qf[G][8];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    const uint4 u = *reinterpret_cast<const uint4*>(q + (static_cast<long long>(m) * Hq + h * G + g) * D + c * 8);
-    bf16x8_to_f32(u, qf[g]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) qf[g][i] *= scale_log2;
-  }
-  __syncthreads();
-
-  float mrun[G], lrun[G], acc[G][8];
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-    mrun[g] = -INFINITY;
-    lrun[g] = 0.f;
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[g][i] = 0.f;
-  }
-
-  const long long tile_bytes = static_cast<long long>(BS) * D * 2;  // one (slot, head) K tile
-  const int n_sub = nblk * C::kSubPerBlock;
-  for (int t = warp; t < n_sub; t += C::kWarps) {
-    const int jl = t / C::kSubPerBlock, sub = t % C::kSubPerBlock;
-    const int tok0 = (jb0 + jl) * BS + sub * 16;
-    const char* slot = base + static_cast<long long>(s_tbl[jl]) * slot_bytes;
-    const char* kp = slot + h * tile_bytes + sub * 16 * D * 2 + r0 * D * 2 + c * 16;
-    const char* vp = kp + static_cast<long long>(Hl) * tile_bytes;
-    uint4 kr[8], vr[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) kr[k] = ld_stream(kp + k * 2 * D * 2);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) vr[k] = ld_stream(vp + k * 2 * D * 2);
-
-    // ---- scores: s[g] for row = r0 + (c & 14)
-    float s[G];
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float pr[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        float kf[8];
-        bf16x8_to_f32(kr[k], kf);
-        float a = 0.f;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) a = fmaf(qf[g][i], kf[i], a);
-        pr[k] = a;
-      }
-      // butterfly over the 16 lanes sharing r0: 4 + 2 + 1 + 1 shuffles
-      const bool b3 = c & 8, b2 = c & 4, b1 = c & 2;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float send = b3 ? pr[j] : pr[j + 4];
-        const float keep = b3 ? pr[j + 4] : pr[j];
-        pr[j] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-      }
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        const float send = b2 ? pr[j] : pr[j + 2];
-        const float keep = b2 ? pr[j + 2] : pr[j];
-        pr[j] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-      }
-      {
-        const float send = b1 ? pr[0] : pr[1];
-        const float keep = b1 ? pr[1] : pr[0];
-        pr[0] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
-      }
-      pr[0] += __shfl_xor_sync(0xffffffffu, pr[0], 1);
-      const int row = r0 + (c & 14);
-      s[g] = (tok0 + row < sd.kv_len) ? pr[0] : -INFINITY;
-    }
-
-    // ---- online softmax + P.V
-#pragma unroll
-    for (int g = 0; g < G; ++g) {
-      float mt = s[g];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) mt = fmaxf(mt, __shfl_xor_sync(0xffffffffu, mt, o));
-      const float mnew = fmaxf(mrun[g], mt);
-      const float corr = (mrun[g] == -INFINITY) ? 0.f : exp2f(mrun[g] - mnew);
-      const float p = (s[g] == -INFINITY) ? 0.f : exp2f(s[g] - mnew);
-      lrun[g] = lrun[g] * corr + ((c & 1) ? 0.f : p);
-      mrun[g] = mnew;
-#pragma unroll
-      for (int i = 0; i < 8; ++i) acc[g][i] *= corr;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float pk = __shfl_sync(0xffffffffu, p, (lane & 16) + 2 * k);
-        float vf[8];
-        bf16x8_to_f32(vr[k], vf);
-#pragma unroll
-        for (int i = 0; i < 8; ++i) acc[g][i] = fmaf(pk, vf[i], acc[g][i]);
-      }
-    }
-  }
-
-  // ---- warp reduce: rows split across r0 halves; l across all lanes
-#pragma unroll
-  for (int g = 0; g < G; ++g) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) acc[g][i] += __shfl_xor_sync(0xffffffffu, acc[g][i], 16);
-    float l = lrun[g];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (lane < 16) {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) s_acc[warp][g][c * 8 + i] = acc[g][i];
-    }
-    if (lane == 0) {
-      s_m[warp][g] = mrun[g];
-      s_l[warp][g] = l;
-    }
-  }
-  __syncthreads();
-
-  // ---- CTA merge of the warps, then final output or split partial
-  for (int idx = threadIdx.x; idx < G * D; idx += C::kThreads) {
-    const int g = idx / D, d = idx % D;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < C::kWarps; ++w) M = fmaxf(M, s_m[w][g]);
-    float o = 0.f, L = 0.f;
-    if (M != -INFINITY) {
-#pragma unroll
-      for (int w = 0; w < C::kWarps; ++w) {
-        const float f = (s_m[w][g] == -INFINITY) ? 0.f : exp2f(s_m[w][g] - M);
-        o += f * s_acc[w][g][d];
-        L += f * s_l[w][g];
-      }
-    }
-    const long long hq = static_cast<long long>(m) * Hq + h * G + g;
-    if (n_split == 1) {
-      store_out(out, out_f32, hq * D + d, L > 0.f ? o / L : 0.f);
-    } else {
-      part_o[(hq * n_split + split) * D + d] = o;
-      if (d == 0) {
-        part_ml[(hq * n_split + split) * 2 + 0] = M;
-        part_ml[(hq * n_split + split) * 2 + 1] = L;
-      }
-    }
-  }
-}
-
-// Combine split partials: o = sum_s 2^(m_s - M) o_s / sum_s 2^(m_s - M) l_s.
-__global__ void decode_merge_kernel(const float* __restrict__ part_o,
-                                    const float* __restrict__ part_ml, int n_split, int D,
-                                    void* __restrict__ out, int out_f32) {
-  const long long hq = blockIdx.x;
-  const int d = threadIdx.x;
-  const float* ml = part_ml + hq * n_split * 2;
-  float M = -INFINITY;
-  for (int s = 0; s < n_split; ++s) M = fmaxf(M, ml[2 * s]);
-  float o = 0.f, L = 0.f;
-  if (M != -INFINITY) {
-    for (int s = 0; s < n_split; ++s) {
-      const float ms = ml[2 * s];
-      if (ms == -INFINITY) continue;
-      const float f = exp2f(ms - M);
-      o += f * part_o[(hq * n_split + s) * D + d];
-      L += f * ml[2 * s + 1];
-    }
-  }
-  if (d < D) store_out(out, out_f32, hq * D + d, L > 0.f ? o / L : 0.f);
 }
 
 // ---------------------------------------------------------------------------

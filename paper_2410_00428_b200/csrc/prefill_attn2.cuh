@@ -1,13 +1,13 @@
-// Causal GQA prefill attention, two query tiles per CTA.
+// Causal GQA prefill attention on tcgen05: the
+// per-layer compute that a layer's offload D2H hides behind
+// (engine.cpp:27-31, schedule_prefill_span). The only place on the path where
+// the work is a dense contraction, so the only tensor-core kernel besides the
+// GQA decode tile.
 //
-// prefill_attn_kernel splits each S row between two softmax warpgroups; both
-// pass the load -> max -> exp -> store phases of one tile in lockstep, so the
-// MUFU (ex2) idles outside the exp phase and the tensor pipe waits on it
-// (ncu: both ~50% busy). Here a CTA owns query tiles A = 2p and B = 2p + 1
-// of one head and gives each its own softmax warpgroup (thread = query row,
-// all 128 columns), so one tile's exponentials overlap the other's TMEM
-// traffic and the MMAs of the other tile, and every K/V tile loaded from HBM
-// serves 256 query rows.
+// A CTA owns query tiles A = 2p and B = 2p + 1 of one head and gives each its
+// own softmax warpgroup (thread = query row, all 128 columns), so one tile's
+// exponentials overlap the other's TMEM traffic and the MMAs of the other
+// tile, and every K/V tile loaded from HBM serves 256 query rows.
 //
 // Warps: 0 TMA (Q_A, Q_B, then the K and V rings, 2 stages each; a K stage
 // frees when both S MMAs read it, a V stage when both PVs did), 1 MMA issuer
@@ -20,6 +20,13 @@
 // The tensor pipe executes in issue order, so S_A(j) never overwrites P_A(j-1)
 // before PV_A(j-1) read it. Tile A's causal range is KV tiles 0..2p, B's is
 // 0..2p+1 (the last KV tile is B's alone).
+//
+// P precision: bf16 P alone misses the 1e-3 bar (2^-9 per weight), so P is
+// fp16 (2^-11) against an fp16 copy of V made by lkv_prefill_attention
+// (bf16_to_f16_kernel; kind::f16 needs A and B in the same format). Lazy
+// rescaling: the running max only moves when a tile exceeds it by more than
+// 2^8; only then does the warp wait for the previous PV and rescale its O
+// columns in TMEM.
 #pragma once
 
 #include <cuda_bf16.h>
@@ -28,7 +35,6 @@
 
 #include <cstdint>
 
-#include "prefill_attn.cuh"
 #include "tc_sm100.cuh"
 
 namespace lkv {
@@ -44,6 +50,13 @@ struct PrefillAttn2Smem {
   static constexpr int kBytes = kTmem + 16;
   static_assert(kBytes <= 232448, "227 KiB dynamic smem limit");
 };
+
+// 2^x on the MUFU pipe, flushing denormals (-inf -> +0).
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // 2^x on the FMA/ALU pipes (x <= ~126): round-to-nearest split x = n + f
 // with the 1.5*2^23 trick, a degree-3 fit of 2^f on [-0.5, 0.5] (max relative
@@ -248,7 +261,7 @@ __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
       const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
       float corr = 1.f;
       bool resc = false;
-      if (mt > m_run + 8.f) {  // lazy rescale (see prefill_attn.cuh)
+      if (mt > m_run + 8.f) {  // lazy rescale
         corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
         resc = j > 0;
         m_run = mt;

@@ -1,5 +1,5 @@
 // sm_100a tensor-core plumbing shared by the GQA tiles (decode_gqa_tc.cuh,
-// prefill_attn.cuh): TMEM allocation, tcgen05.mma issue/commit, TMEM loads,
+// prefill_attn2.cuh): TMEM allocation, tcgen05.mma issue/commit, TMEM loads,
 // UMMA shared-memory / instruction descriptors and TMA tensor copies.
 //
 // Descriptor encodings (PTX ISA "Matrix Descriptors" for tcgen05):

@@ -66,7 +66,7 @@ def main():
             kres.append(st.attn_ms / st.attn_launches)
     kvb = a.batch * a.ctx * 2 * hkv * 128 * 2
     ms = min(res)
-    print(json.dumps({"variant": os.environ.get("LKV_V2_CFG", "default"), "merge": os.environ.get("LKV_MERGE", "5"),
+    print(json.dumps({"variant": "default",
                       "offloaded": a.offloaded, "idle_ms": a.idle_ms, "merge_ms": ms - min(kres),
                       "group": a.group, "hkv": hkv, "batch": a.batch, "ctx": a.ctx, "bs": a.bs,
                       "ms_per_layer": ms, "kernel_ms": min(kres), "kernel_ms_mean": sum(kres) / len(kres), "kernel_span_ms": min(kspan), "GBps": kvb / (ms / 1e3) / 1e9,

@@ -26,10 +26,7 @@ def main():
     p.add_argument("--iters", type=int, default=20)
     p.add_argument("--group", type=int, default=1)
     p.add_argument("--bs", type=int, default=16)
-    p.add_argument("--kernel", type=int, default=0)
     a = p.parse_args()
-    if a.kernel:
-        os.environ["LKV_DECODE_KERNEL"] = str(a.kernel)
     re = oracle.restatement()
     fails = 0
     for it in range(a.iters):

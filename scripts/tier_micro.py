@@ -22,7 +22,6 @@ def main():
     dev = torch.device("cuda:0")
     link = bench.host_link_peak(torch, dev)
     row = bench.tiered_host_row(torch, dev, link, pinned_frac=a.pinned_frac)
-    row["env_LKV_TIER_NT"] = os.environ.get("LKV_TIER_NT", "1")
     print(json.dumps(row))
 
 

@@ -92,13 +92,11 @@ def test_attention_parity_ragged(group, bs):
     sc.check_attention(dev, list(range(len(lens))), lens)
 
 
-@pytest.mark.parametrize("kernel", [1, 2, 3])
-@pytest.mark.parametrize("group,bs", [(1, 16), (2, 32), (4, 16), (8, 16), (8, 64)])
-def test_attention_parity_each_kernel(kernel, group, bs, monkeypatch):
-    """Every decode kernel (split-K CUDA core, persistent TMA-bulk CUDA core,
-    tcgen05 GQA tile) against the fp32 oracle on ragged lengths, including
-    chunks that end mid-tile and a sequence longer than one chunk."""
-    monkeypatch.setenv("LKV_DECODE_KERNEL", str(kernel))
+@pytest.mark.parametrize("group,bs", [(1, 16), (1, 32), (2, 32), (4, 16), (8, 16), (8, 64)])
+def test_attention_parity_each_kernel(group, bs):
+    """Both decode kernels (G = 1: persistent TMA-bulk CUDA-core kernel;
+    G >= 2: tcgen05 GQA tile) against the fp32 oracle on ragged lengths,
+    including chunks that end mid-tile and a sequence longer than one chunk."""
     model = sc.gqa_model(L=2, hkv=4, group=group)
     kv, dev = sc.make(model, bs=bs, gpu=4000, cpu=4000, max_blocks=640, arena=4000)
     lens = [1, 100, 129, 2 * bs + 3, 5000]
@@ -107,13 +105,11 @@ def test_attention_parity_each_kernel(kernel, group, bs, monkeypatch):
     sc.check_attention(dev, list(range(len(lens))), lens)
 
 
-@pytest.mark.parametrize("merge", [3, 4, 5])
 @pytest.mark.parametrize("group", [1, 8])
-def test_attention_parity_each_merge(merge, group, monkeypatch):
-    """Every split merge (warp per head, two-pass 4 warps, single-pass 8
-    warps with per-warp running max) on members with 1 to ~300 chunks, so
-    batches cross the running-max rescale and warps see empty chunk lists."""
-    monkeypatch.setenv("LKV_MERGE", str(merge))
+def test_attention_parity_merge_many_chunks(group):
+    """The split merge (single pass, 4 warps, per-warp running max) on members
+    with 1 to ~300 chunks, so batches cross the running-max rescale and warps
+    see empty chunk lists."""
     model = sc.gqa_model(L=2, hkv=2, group=group)
     kv, dev = sc.make(model, gpu=9000, cpu=9000, max_blocks=4096, arena=9000)
     lens = [1, 40, 3000, 40000]
