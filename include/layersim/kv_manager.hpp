@@ -233,9 +233,9 @@ class KvManager {
     std::int64_t next_fresh_ = 0;
     std::vector<std::uint32_t> pushed_;
     std::vector<std::uint64_t> held_bits_;  // grows with next_fresh_
-    // journal state of the device mirror: lowest pushed_.size() and
-    // next_fresh_ since the last take_delta
-    std::int64_t low_ = 0, fresh_taken_ = 0;
+    // journal state of the device mirror: lowest pushed_.size() since the
+    // last take_delta, and next_fresh_ / pushed_.size() at that take
+    std::int64_t low_ = 0, fresh_taken_ = 0, size_taken_ = 0;
   };
 
   struct Table {

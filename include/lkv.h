@@ -176,6 +176,14 @@ LKV_API int lkv_kv_dump_hash(const lkv_kv_manager*, uint64_t* out);
  * whole stack bottom to top (next alloc = last). *size = free slots; the stack
  * is written to out when cap >= *size. */
 LKV_API int lkv_kv_free_stack(const lkv_kv_manager*, int32_t which, uint32_t* out, int64_t cap, int64_t* size);
+/* The free-list journal the device mirror consumes (lkv_device_bind owns it
+ * while a device is bound; call it only on an unbound manager): the change
+ * since the previous take as {next_fresh, low, size, changed} plus the
+ * pushed entries [low, size), written to out when cap >= size - low. A
+ * mirror applies it as: stack = [total-1 ... next_fresh] + pushed[0..size),
+ * with pushed[low..size) replaced. full = 1 restarts from low = 0. */
+LKV_API int lkv_kv_free_delta(lkv_kv_manager*, int32_t which, int32_t full, int64_t* next_fresh, int64_t* low,
+                              int64_t* size, int32_t* changed, uint32_t* out, int64_t cap);
 
 /* ---- PcieBus, parity-mode timing (reference interconnect.hpp:9-80) ------ */
 typedef struct lkv_pcie_bus lkv_pcie_bus;

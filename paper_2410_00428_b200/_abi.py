@@ -165,6 +165,7 @@ _PROTOS = {
     "lkv_kv_dump_table": [vp, C.c_char_p, C.c_size_t, P(C.c_size_t)],
     "lkv_kv_dump_hash": [vp, P(u64)],
     "lkv_kv_free_stack": [vp, i32, P(u32), i64, P(i64)],
+    "lkv_kv_free_delta": [vp, i32, i32, P(i64), P(i64), P(i64), P(i32), P(u32), i64],
     "lkv_bus_create": [f64, P(vp)],
     "lkv_bus_destroy": [vp],
     "lkv_bus_register_allreduce": [vp, f64, f64, P(HardwareSpec)],

@@ -418,6 +418,18 @@ int lkv_kv_free_stack(const lkv_kv_manager* kv, int32_t which, uint32_t* out, in
   LKV_CATCH
 }
 
+int lkv_kv_free_delta(lkv_kv_manager* kv, int32_t which, int32_t full, int64_t* next_fresh, int64_t* low,
+                      int64_t* size, int32_t* changed, uint32_t* out, int64_t cap) {
+  LKV_REQUIRE(kv && (which == 0 || which == 1) && next_fresh && low && size && changed && (out || cap == 0));
+  LKV_TRY const auto d = kv->impl.take_free_delta(which == 0, full != 0);
+  *next_fresh = d.next_fresh;
+  *low = d.low;
+  *size = d.size;
+  *changed = d.changed ? 1 : 0;
+  if (cap >= d.size - d.low) std::copy(d.pushed + d.low, d.pushed + d.size, out);
+  LKV_CATCH
+}
+
 int lkv_kv_dump_hash(const lkv_kv_manager* kv, uint64_t* out) {
   LKV_REQUIRE(kv && out);
   LKV_TRY std::ostringstream os;

@@ -26,6 +26,7 @@
 #include "decode_attn.cuh"
 #include "decode_gqa_tc.cuh"
 #include "prefill_attn2.cuh"
+#include "host_mem.hpp"
 #include "host_tier.hpp"
 #include "kernels.cuh"
 #include "layersim/errors.hpp"
@@ -130,6 +131,8 @@ struct lkv_device final : layersim::KvObserver {
   // ---- memory
   char* dbuf = nullptr;        // pool | arena stages
   char* host_pool = nullptr;   // pinned, CPU slot frames (tiered: the pinned frame tier)
+  PinnedHost host_mem;         // host_pool's pages (untiered), on the GPU's NUMA node
+  int numa_node = -1;          // the GPU's NUMA node (sysfs), -1 unknown
   // ---- tiered host memory: pageable homes + pinned frames
   HostTier tier;
   int* d_xlat = nullptr;        // [host_slots] CPU slot -> pinned frame (verify/fill kernels)
@@ -280,14 +283,15 @@ struct lkv_device final : layersim::KvObserver {
     if (frames > 0x7FFFFFFFll) throw CapacityError("pool + arena frames exceed int32 indexing");
     LKV_CUDA(cudaMalloc(&dbuf, std::max<long long>(frames, 1) * sb));
 
+    numa_node = gpu_numa_node(cfg.device);
+    const int cores = static_cast<int>(std::thread::hardware_concurrency());
     if (cfg.pinned_frames > 0 && cfg.host_slots > 0) {  // tiered: homes pageable, frames pinned
-      const int cores = static_cast<int>(std::thread::hardware_concurrency());
-      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb, std::clamp(cores, 2, 16));
+      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb, std::clamp(cores, 2, 16), numa_node);
       host_pool = tier.pinned();
       LKV_CUDA(cudaMalloc(&d_xlat, cfg.host_slots * sizeof(int)));
     } else if (cfg.host_slots > 0) {
-      LKV_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&host_pool), cfg.host_slots * sb,
-                             cudaHostAllocMapped | cudaHostAllocPortable));
+      host_mem.allocate(static_cast<std::size_t>(cfg.host_slots * sb), numa_node, std::clamp(cores, 1, 32));
+      host_pool = host_mem.data();
     }
     const long long tbl = static_cast<long long>(cfg.max_requests) * L * cfg.max_blocks;
     // SeqDesc::row_offset and the snapshot kernel index the table in int32
@@ -392,7 +396,7 @@ struct lkv_device final : layersim::KvObserver {
     for (auto& kvp : prefill_ev) cudaEventDestroy(kvp.second);
     ring.destroy();
     cudaFree(dbuf);
-    if (host_pool && !tiered()) cudaFreeHost(host_pool);
+    host_mem.release();
     tier.destroy();
     cudaFree(d_xlat);
     cudaFree(d_table);

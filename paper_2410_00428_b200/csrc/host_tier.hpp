@@ -11,23 +11,30 @@
 //     lands in the slot's pinned frame; the frame is dirty until the cleaner
 //     thread copies it home after the GPU work's event completes;
 //   - an H2D prefetch or an in-kernel read needs the slot resident: a
-//     missing slot is read in from its home (parallel memcpy) into a frame
-//     before the copy is enqueued;
+//     missing slot is read in from its home into a frame by a persistent
+//     pool of copy workers. stage() starts those read-ins without waiting
+//     (the decode path stages layers several ahead of their DMA), pin()
+//     waits only for the ones still running;
 //   - a frame is reused least-recently-used first, never before its last
-//     GPU use completed, and never while dirty (written back first);
+//     GPU use completed, never while locked (pinned or staged), being read
+//     in or written home, and never while dirty (written back first);
 //   - slots the manager frees are forgotten (no write-back).
-// Single writer (the device's API thread) + the cleaner thread, one mutex.
+// Homes and frames sit on the GPU's NUMA node. One mutex guards the frame
+// table; the API thread, the cleaner and the copy workers take it briefly.
 #pragma once
 
 #include <cuda_runtime.h>
 #include <emmintrin.h>
 #include <sys/mman.h>
+#include <sys/syscall.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <list>
 #include <memory>
 #include <mutex>
@@ -36,10 +43,14 @@
 #include <thread>
 #include <vector>
 
+#include "host_mem.hpp"
+
 namespace lkv {
 
 struct HostTierStats {
   long long read_in_frames = 0, write_back_frames = 0, evictions = 0, hits = 0, misses = 0;
+  long long staged = 0;      // slots staged ahead of their pin()
+  long long pin_waits = 0;   // pin() calls that waited for a read-in still running
 };
 
 class HostTier {
@@ -50,7 +61,7 @@ class HostTier {
   ~HostTier() { destroy(); }
 
   // slots: addressable CPU slots (pageable homes); frames: pinned frames.
-  void init(int device, long long slots, long long frames, long long frame_bytes, int copy_threads = 8) {
+  void init(int device, long long slots, long long frames, long long frame_bytes, int copy_threads, int numa_node) {
     device_ = device;
     S_ = slots;
     F_ = frames;
@@ -62,31 +73,43 @@ class HostTier {
     // 2 MiB pages where the kernel allows them (THP "madvise" or "always"):
     // a 256 KiB frame copy touches 64 base pages otherwise.
     madvise(home_, static_cast<std::size_t>(S_ * sb_), MADV_HUGEPAGE);
-    cudaError_t e = cudaHostAlloc(reinterpret_cast<void**>(&pinned_), static_cast<std::size_t>(F_ * sb_),
-                                  cudaHostAllocMapped | cudaHostAllocPortable);
-    if (e != cudaSuccess) throw std::runtime_error(std::string("host tier: cudaHostAlloc: ") + cudaGetErrorString(e));
+    if (numa_node >= 0 && numa_node < 128) {  // homes follow the frames (pages are placed at first write)
+      unsigned long mask[2] = {0ul, 0ul};
+      mask[numa_node / 64] = 1ul << (numa_node % 64);
+      syscall(SYS_mbind, home_, static_cast<std::size_t>(S_ * sb_), 1l /* MPOL_PREFERRED */, mask, 129ul, 0u);
+    }
+    threads_ = std::max(1, copy_threads);
+    pinned_mem_.allocate(static_cast<std::size_t>(F_ * sb_), numa_node, threads_);
+    pinned_ = pinned_mem_.data();
     slot_frame_.assign(static_cast<std::size_t>(S_), -1);
     slot_valid_.assign(static_cast<std::size_t>(S_), 0);
     frames_.resize(static_cast<std::size_t>(F_));
     // popped from the back: ascending frames, so a batch of misses gets a
     // contiguous run and its DMA coalesces into one copy
     for (long long f = F_ - 1; f >= 0; --f) free_.push_back(static_cast<int>(f));
-    threads_ = std::max(1, copy_threads);
     stop_ = false;
+    for (int i = 0; i < threads_; ++i) workers_.emplace_back([this] { work_loop(); });
     cleaner_ = std::thread([this] { clean_loop(); });
   }
 
   void destroy() {
-    if (cleaner_.joinable()) {
+    if (cleaner_.joinable() || !workers_.empty()) {
       {
         std::lock_guard<std::mutex> g(mu_);
         stop_ = true;
       }
+      {
+        std::lock_guard<std::mutex> g(qmu_);
+        qstop_ = true;
+      }
       cv_.notify_all();
-      cleaner_.join();
+      qcv_.notify_all();
+      if (cleaner_.joinable()) cleaner_.join();
+      for (auto& t : workers_) t.join();
+      workers_.clear();
     }
     frames_.clear();
-    if (pinned_) cudaFreeHost(pinned_);
+    pinned_mem_.release();
     pinned_ = nullptr;
     if (home_) munmap(home_, static_cast<std::size_t>(S_ * sb_));
     home_ = nullptr;
@@ -95,44 +118,75 @@ class HostTier {
   bool enabled() const { return pinned_ != nullptr; }
   char* pinned() const { return pinned_; }
   long long frames() const { return F_; }
+  int numa_node() const { return pinned_mem_.node(); }
   HostTierStats stats() const {
     std::lock_guard<std::mutex> g(mu_);
     return st_;
   }
 
+  // Read-ahead: make `slots` resident, starting the read-in of missing ones
+  // on the copy workers without waiting for them. Every slot keeps one stage
+  // lock (no eviction) until a pin() consumes it or unstage() drops it.
+  void stage(const long long* slots, long long n) {
+    std::vector<Job> jobs;
+    {
+      std::unique_lock<std::mutex> g(mu_);
+      for (long long i = 0; i < n; ++i) {
+        bool fill = false;
+        const int f = resident_or_take(g, slots[i], &fill);
+        Frame& fr = frames_[static_cast<std::size_t>(f)];
+        fr.stage_locks += 1;
+        if (fill) jobs.push_back(fill_job(f));
+      }
+      st_.staged += n;
+    }
+    submit(jobs);
+  }
+  // Drops stage locks that no pin() consumed (an iteration that ended early).
+  void unstage(const long long* slots, long long n) {
+    std::lock_guard<std::mutex> g(mu_);
+    for (long long i = 0; i < n; ++i) {
+      const long long s = slots[i];
+      if (s < 0 || s >= S_) continue;
+      const int f = slot_frame_[static_cast<std::size_t>(s)];
+      if (f >= 0 && frames_[static_cast<std::size_t>(f)].stage_locks > 0) frames_[static_cast<std::size_t>(f)].stage_locks -= 1;
+    }
+    cv_.notify_all();
+  }
+
   // Frames for `n` slots, locked against eviction until the matching used()
-  // call. read: the frame must hold the slot's current bytes.
+  // call (a stage lock, if any, becomes that lock). read: the frame must hold
+  // the slot's current bytes: waits for read-ins still running and reads in
+  // the slots that were not staged.
   void pin(const long long* slots, long long n, bool read, long long* frames_out) {
+    std::vector<Job> jobs;
     std::unique_lock<std::mutex> g(mu_);
-    std::vector<std::pair<long long, int>> fills;  // (slot, frame) to read in
     for (long long i = 0; i < n; ++i) {
       const long long s = slots[i];
       if (s < 0 || s >= S_) throw std::out_of_range("host tier: CPU slot " + std::to_string(s));
-      int f = slot_frame_[static_cast<std::size_t>(s)];
-      if (f >= 0) {
-        ++st_.hits;
-        touch(f);
-      } else {
-        ++st_.misses;
-        f = take_frame(g);
-        Frame& fr = frames_[static_cast<std::size_t>(f)];
-        fr.slot = s;
-        slot_frame_[static_cast<std::size_t>(s)] = f;
-        lru_.push_back(f);
-        fr.pos = std::prev(lru_.end());
-        fr.in_lru = true;
-        if (read && slot_valid_[static_cast<std::size_t>(s)]) fills.emplace_back(s, f);
-      }
-      frames_[static_cast<std::size_t>(f)].locks += 1;
+      const int f0 = slot_frame_[static_cast<std::size_t>(s)];
+      const bool staged = f0 >= 0 && frames_[static_cast<std::size_t>(f0)].stage_locks > 0;  // counted by stage()
+      bool fill = false;
+      const int f = resident_or_take(g, s, &fill, read, !staged);
+      Frame& fr = frames_[static_cast<std::size_t>(f)];
+      if (fr.stage_locks > 0) fr.stage_locks -= 1;
+      fr.locks += 1;
+      if (fill) jobs.push_back(fill_job(f));
       frames_out[i] = f;
     }
     g.unlock();
-    if (!fills.empty()) {  // pageable homes -> pinned frames, in parallel
-      copy_parallel(fills.size(), [&](std::size_t k) {
-        copy_frame(pinned_ + fills[k].second * sb_, home_ + fills[k].first * sb_, static_cast<std::size_t>(sb_));
-      });
-      std::lock_guard<std::mutex> g2(mu_);
-      st_.read_in_frames += static_cast<long long>(fills.size());
+    submit(jobs);
+    // a staged read-in still running must land before the caller reads the
+    // frame, or before a GPU write replaces it (else it would overwrite it)
+    g.lock();
+    auto filling = [&] {
+      for (long long i = 0; i < n; ++i)
+        if (frames_[static_cast<std::size_t>(frames_out[i])].filling) return true;
+      return false;
+    };
+    if (filling()) {
+      ++st_.pin_waits;
+      cv_.wait(g, [&] { return !filling(); });
     }
   }
 
@@ -147,13 +201,14 @@ class HostTier {
       Frame& fr = frames_[static_cast<std::size_t>(f)];
       fr.last = ticket;
       if (write) {
+        if (!fr.dirty) dirty_q_.push_back(f);
         fr.dirty = true;
         fr.gen += 1;  // a copy home that started before this write does not clean it
         slot_valid_[static_cast<std::size_t>(slots[i])] = 1;
       }
       if (fr.locks > 0) fr.locks -= 1;
     }
-    if (write) cv_.notify_all();
+    cv_.notify_all();
   }
 
   // The manager freed these slots: drop their bytes (no write-back).
@@ -166,11 +221,14 @@ class HostTier {
       const int f = slot_frame_[static_cast<std::size_t>(s)];
       if (f < 0) continue;
       Frame& fr = frames_[static_cast<std::size_t>(f)];
-      while (fr.cleaning) cv_.wait(g);  // the cleaner's copy of now-dead bytes finishes first
+      // a copy of now-dead bytes (home or in) finishes first
+      cv_.wait(g, [&] { return !fr.cleaning && !fr.filling; });
       if (slot_frame_[static_cast<std::size_t>(s)] != f) continue;
       fr.dirty = false;
+      fr.stage_locks = 0;
       release_frame(f);
     }
+    cv_.notify_all();
   }
 
   // Copy one slot's current bytes (resident or home) to `dst` (tests).
@@ -178,7 +236,9 @@ class HostTier {
     std::unique_lock<std::mutex> g(mu_);
     const int f = slot_frame_[static_cast<std::size_t>(s)];
     if (f >= 0) {
-      auto t = frames_[static_cast<std::size_t>(f)].last;
+      Frame& fr = frames_[static_cast<std::size_t>(f)];
+      cv_.wait(g, [&] { return !fr.filling; });
+      auto t = fr.last;
       g.unlock();
       if (t) cudaEventSynchronize(t->ev);
       std::memcpy(dst, pinned_ + f * sb_, static_cast<std::size_t>(sb_));
@@ -189,11 +249,9 @@ class HostTier {
 
  private:
   struct Ticket {
-    explicit Ticket(cudaEvent_t src) {
-      // own a copy of the completion point: record-after is not available,
-      // so the caller's event handle is kept and never re-recorded by it.
-      ev = src;
-    }
+    // Owns the caller's event handle (recorded after the GPU work, never
+    // re-recorded by it).
+    explicit Ticket(cudaEvent_t src) : ev(src) {}
     ~Ticket() {
       if (ev) cudaEventDestroy(ev);
     }
@@ -201,12 +259,48 @@ class HostTier {
   };
   struct Frame {
     long long slot = -1;
-    bool dirty = false, cleaning = false, in_lru = false;
-    int locks = 0;
+    bool dirty = false, cleaning = false, filling = false, in_lru = false;
+    int locks = 0, stage_locks = 0;
     unsigned gen = 0;  // write generation
     std::shared_ptr<Ticket> last;
     std::list<int>::iterator pos;
   };
+  struct Job {
+    char* dst;
+    const char* src;
+    int frame;  // read-in: clears filling; -1: none
+  };
+
+  Job fill_job(int f) const {
+    const Frame& fr = frames_[static_cast<std::size_t>(f)];
+    return {pinned_ + f * sb_, home_ + fr.slot * sb_, f};
+  }
+
+  // The slot's frame, making it resident (a fresh frame) when needed; *fill
+  // = a read-in must be started (read and the slot holds bytes). Called
+  // with mu_ held.
+  int resident_or_take(std::unique_lock<std::mutex>& g, long long s, bool* fill, bool read = true,
+                       bool count = true) {
+    if (s < 0 || s >= S_) throw std::out_of_range("host tier: CPU slot " + std::to_string(s));
+    int f = slot_frame_[static_cast<std::size_t>(s)];
+    if (f >= 0) {
+      if (count) ++st_.hits;
+      touch(f);
+      *fill = false;
+      return f;
+    }
+    if (count) ++st_.misses;
+    f = take_frame(g);
+    Frame& fr = frames_[static_cast<std::size_t>(f)];
+    fr.slot = s;
+    slot_frame_[static_cast<std::size_t>(s)] = f;
+    lru_.push_back(f);
+    fr.pos = std::prev(lru_.end());
+    fr.in_lru = true;
+    *fill = read && slot_valid_[static_cast<std::size_t>(s)];
+    fr.filling = *fill;
+    return f;
+  }
 
   void touch(int f) {
     Frame& fr = frames_[static_cast<std::size_t>(f)];
@@ -231,8 +325,12 @@ class HostTier {
     }
   }
 
-  // A free frame, evicting the least recently used unlocked one (its GPU use
-  // completed; written home first when dirty). Called with mu_ held.
+  static bool evictable(const Frame& fr) {
+    return fr.locks == 0 && fr.stage_locks == 0 && !fr.cleaning && !fr.filling;
+  }
+
+  // A free frame, evicting the least recently used evictable one (its GPU
+  // use completed; written home first when dirty). Called with mu_ held.
   int take_frame(std::unique_lock<std::mutex>& g) {
     for (;;) {
       if (!free_.empty()) {  // a freed frame may still be read by an in-flight copy
@@ -249,18 +347,19 @@ class HostTier {
         return f;
       }
       int victim = -1;
-      for (int f : lru_) {
-        const Frame& fr = frames_[static_cast<std::size_t>(f)];
-        if (fr.locks == 0 && !fr.cleaning) {
+      for (int f : lru_)
+        if (evictable(frames_[static_cast<std::size_t>(f)])) {
           victim = f;
           break;
         }
-      }
       if (victim < 0) {
-        bool any_cleaning = false;
-        for (int f : lru_) any_cleaning |= frames_[static_cast<std::size_t>(f)].cleaning;
-        if (!any_cleaning)
-          throw std::length_error("host tier: every pinned frame is locked by the current batch (raise pinned_frames)");
+        bool busy = false;  // something that will make a frame evictable without this thread
+        for (int f : lru_) {
+          const Frame& fr = frames_[static_cast<std::size_t>(f)];
+          busy |= fr.cleaning || fr.filling;
+        }
+        if (!busy)
+          throw std::length_error("host tier: every pinned frame is locked by work in flight (raise pinned_frames)");
         cv_.wait(g);
         continue;
       }
@@ -272,14 +371,18 @@ class HostTier {
       wait_ticket(t);
       g.lock();
       fr.locks -= 1;
+      if (!evictable(fr) || fr.slot != s) continue;  // re-locked meanwhile (a stage/pin of the same slot)
       if (fr.dirty) {  // the cleaner has not reached it: write it home here
         fr.cleaning = true;
+        const unsigned gen = fr.gen;
         g.unlock();
         copy_frame(home_ + s * sb_, pinned_ + victim * sb_, static_cast<std::size_t>(sb_));
         g.lock();
         fr.cleaning = false;
-        fr.dirty = false;
+        if (fr.gen == gen) fr.dirty = false;
         ++st_.write_back_frames;
+        cv_.notify_all();
+        if (fr.dirty || !evictable(fr) || fr.slot != s) continue;
       }
       ++st_.evictions;
       release_frame(victim);
@@ -287,23 +390,61 @@ class HostTier {
     }
   }
 
+  // ---- copy workers (persistent; read-ins of stage() and pin())
+  void submit(const std::vector<Job>& jobs) {
+    if (jobs.empty()) return;
+    {
+      std::lock_guard<std::mutex> g(qmu_);
+      for (const Job& j : jobs) q_.push_back(j);
+    }
+    if (jobs.size() == 1)
+      qcv_.notify_one();
+    else
+      qcv_.notify_all();
+  }
+
+  void work_loop() {
+    for (;;) {
+      Job j;
+      {
+        std::unique_lock<std::mutex> g(qmu_);
+        qcv_.wait(g, [&] { return qstop_ || !q_.empty(); });
+        if (q_.empty()) return;  // stopping
+        j = q_.front();
+        q_.pop_front();
+      }
+      copy_frame(j.dst, j.src, static_cast<std::size_t>(sb_));
+      if (j.frame >= 0) {
+        std::lock_guard<std::mutex> g(mu_);
+        frames_[static_cast<std::size_t>(j.frame)].filling = false;
+        ++st_.read_in_frames;
+      }
+      cv_.notify_all();
+    }
+  }
+
   // The paper's CPU thread: copy dirty frames whose GPU writes completed to
-  // their pageable homes, oldest first.
+  // their pageable homes, in the order they became dirty.
   void clean_loop() {
     cudaSetDevice(device_);
     std::unique_lock<std::mutex> g(mu_);
     while (!stop_) {
       int pick = -1;
-      for (int f : lru_) {
+      while (!dirty_q_.empty()) {
+        const int f = dirty_q_.front();
         Frame& fr = frames_[static_cast<std::size_t>(f)];
-        if (fr.dirty && !fr.cleaning && fr.locks == 0 &&
-            (!fr.last || !fr.last->ev || cudaEventQuery(fr.last->ev) == cudaSuccess)) {
-          pick = f;
-          break;
+        if (!fr.dirty || fr.cleaning) {  // cleaned or forgotten meanwhile (or being evicted)
+          dirty_q_.pop_front();
+          continue;
         }
+        if (fr.locks == 0 && (!fr.last || !fr.last->ev || cudaEventQuery(fr.last->ev) == cudaSuccess)) {
+          pick = f;
+          dirty_q_.pop_front();
+        }
+        break;
       }
       if (pick < 0) {
-        cv_.wait_for(g, std::chrono::milliseconds(2));
+        cv_.wait_for(g, std::chrono::milliseconds(1));
         continue;
       }
       Frame& fr = frames_[static_cast<std::size_t>(pick)];
@@ -314,7 +455,11 @@ class HostTier {
       copy_frame(home_ + s * sb_, pinned_ + pick * sb_, static_cast<std::size_t>(sb_));
       g.lock();
       fr.cleaning = false;
-      if (fr.gen == gen) fr.dirty = false;  // else written again meanwhile: stays dirty
+      if (fr.gen == gen) {
+        fr.dirty = false;
+      } else {
+        dirty_q_.push_back(pick);  // written again meanwhile: stays dirty
+      }
       ++st_.write_back_frames;
       cv_.notify_all();
     }
@@ -323,8 +468,9 @@ class HostTier {
   // Frame <-> home copy with non-temporal 16-byte stores: a 256 KiB frame
   // is never re-read by the CPU, so skipping the destination's
   // read-for-ownership saves a third of the host DRAM traffic the read-in
-  // shares with the DMA reading the pinned frames.
-  static void stream_copy(char* dst, const char* src, std::size_t n) {
+  // shares with the DMA reading the pinned frames
+  // (profiles/r1y_tier_nt_micro.jsonl).
+  static void copy_frame(char* dst, const char* src, std::size_t n) {
     if (((reinterpret_cast<std::uintptr_t>(dst) | reinterpret_cast<std::uintptr_t>(src) | n) & 63u) != 0u) {
       std::memcpy(dst, src, n);
       return;
@@ -342,43 +488,29 @@ class HostTier {
     _mm_sfence();
   }
 
-  // Non-temporal stores: frames are not re-read by this CPU, so they skip
-  // the cache (profiles/r1y_tier_nt_micro.jsonl).
-  void copy_frame(char* dst, const char* src, std::size_t n) const { stream_copy(dst, src, n); }
-
-  template <class Fn>
-  void copy_parallel(std::size_t n, Fn&& fn) {
-    const int t = static_cast<int>(std::min<std::size_t>(static_cast<std::size_t>(threads_), (n + 3) / 4));
-    if (t <= 1) {
-      for (std::size_t k = 0; k < n; ++k) fn(k);
-      return;
-    }
-    std::atomic<std::size_t> next{0};
-    std::vector<std::thread> pool;
-    pool.reserve(static_cast<std::size_t>(t - 1));
-    auto work = [&] {
-      for (std::size_t k = next.fetch_add(1); k < n; k = next.fetch_add(1)) fn(k);
-    };
-    for (int i = 1; i < t; ++i) pool.emplace_back(work);
-    work();
-    for (auto& th : pool) th.join();
-  }
-
   int device_ = 0;
   long long S_ = 0, F_ = 0, sb_ = 0;
   char* home_ = nullptr;
+  PinnedHost pinned_mem_;
   char* pinned_ = nullptr;
   std::vector<int> slot_frame_;
   std::vector<std::uint8_t> slot_valid_;
   std::vector<Frame> frames_;
   std::vector<int> free_;
   std::list<int> lru_;
+  std::deque<int> dirty_q_;
   mutable std::mutex mu_;
   std::condition_variable cv_;
   std::thread cleaner_;
   bool stop_ = false;
   int threads_ = 8;
   HostTierStats st_;
+  // copy workers
+  std::vector<std::thread> workers_;
+  std::deque<Job> q_;
+  std::mutex qmu_;
+  std::condition_variable qcv_;
+  bool qstop_ = false;
 };
 
 }  // namespace lkv

@@ -368,6 +368,16 @@ class KvManager:
         self._lib.call("lkv_kv_free_stack", self.handle, which, out, n.value, C.byref(n))
         return list(out)[:n.value]
 
+    def free_delta(self, gpu: bool = True, full: bool = False):
+        """The free-list journal the device mirror applies (include/lkv.h
+        lkv_kv_free_delta): (next_fresh, low, size, changed, pushed[low:size])."""
+        nf, lo, sz, ch = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int32()
+        cap = self.gpu_blocks_total() if gpu else self.cpu_blocks_total()
+        out = (C.c_uint32 * max(1, cap))()
+        self._lib.call("lkv_kv_free_delta", self.handle, 0 if gpu else 1, 1 if full else 0, C.byref(nf), C.byref(lo),
+                       C.byref(sz), C.byref(ch), out, cap)
+        return nf.value, lo.value, sz.value, bool(ch.value), list(out)[:sz.value - lo.value]
+
     def dump_hash(self) -> int:
         h = C.c_uint64()
         self._lib.call("lkv_kv_dump_hash", self.handle, C.byref(h))

@@ -265,3 +265,35 @@ def test_counters_match_full_scans(lib):
         toks = sum(min(max(r.cached_tokens - b.token_begin, 0), 16) for b in r.blocks
                    if b.layers[job.layer].loc == LOC_CPU)
         assert job.bytes == toks * ls.kv_bytes_per_token_layer(m, lib=lib)
+
+
+def test_free_delta_journal_replays_the_stacks():
+    """a4: the free-list journal the device mirror applies (lkv_kv_free_delta)
+    rebuilds both LIFO stacks exactly when replayed into a host-side mirror
+    after every op of the Rng(31) fuzz (escalations, completions, orphaned
+    releases) — including steps whose only change is a pop from the pushed
+    part (the stack shrinks with nothing to upload: the header must still
+    change; round 1's journal missed exactly that)."""
+    from tests import _drivers as drv
+    mirrors = []
+
+    def bind(kv):
+        total = {True: kv.gpu_blocks_total(), False: kv.cpu_blocks_total()}
+        state = {g: {"fresh": 0, "pushed": []} for g in (True, False)}
+        first = [True]
+
+        def check(step):
+            for g in (True, False):
+                nf, lo, sz, changed, entries = kv.free_delta(g, full=first[0])
+                st = state[g]
+                if changed:
+                    st["fresh"] = nf
+                    st["pushed"] = st["pushed"][:lo] + entries
+                    assert len(st["pushed"]) == sz
+                mirror = list(range(total[g] - 1, st["fresh"] - 1, -1)) + st["pushed"]
+                assert mirror == kv.free_stack(g), (step, g)
+            first[0] = False
+            mirrors.append(step)
+        return check
+    drv.fuzz_ops(None, seed=31, rounds=3, steps=300, on_kv=bind)
+    assert len(mirrors) == 3 * 301
