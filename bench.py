@@ -137,7 +137,25 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ host link peak
-def host_link_peak(torch, dev):
+def host_link_peak(torch, dev, world=1):
+    """Pinned cudaMemcpyAsync GB/s per direction on this GPU alone, and —
+    with world > 1 — with every rank copying at the same moment (a barrier
+    before each direction; SURVEY §8d "all 8 GPUs concurrently")."""
+    out = _link_copy(torch, dev)
+    if world > 1:
+        import torch.distributed as dist
+        conc = _link_copy(torch, dev, barrier=dist.barrier)
+        both = torch.tensor([conc["h2d"], conc["d2h"]], dtype=torch.float64)
+        tot, low = both.clone(), both.clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        dist.all_reduce(low, op=dist.ReduceOp.MIN)
+        out["concurrent"] = {"ranks": world, "h2d_gbs_this_rank": conc["h2d"], "d2h_gbs_this_rank": conc["d2h"],
+                             "h2d_gbs_sum": float(tot[0]), "d2h_gbs_sum": float(tot[1]),
+                             "h2d_gbs_min_rank": float(low[0]), "d2h_gbs_min_rank": float(low[1])}
+    return out
+
+
+def _link_copy(torch, dev, barrier=None):
     n = 1 << 30
     h = torch.empty(n, dtype=torch.uint8, pin_memory=True)
     d = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -147,6 +165,9 @@ def host_link_peak(torch, dev):
         for name, fn in (("h2d", lambda: d.copy_(h, non_blocking=True)),
                          ("d2h", lambda: h.copy_(d, non_blocking=True))):
             fn()
+            s.synchronize()
+            if barrier is not None:
+                barrier()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(s)
             for _ in range(4):
@@ -598,8 +619,10 @@ def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=
     CPU slots' homes in pageable memory and only `pinned_frac` of them backed
     by pinned frames. The layer-ordered re-fetch cycles through more slots
     than there are frames, so nearly every prefetch reads its slot back in
-    from the pageable home (parallel memcpy) before the DMA: this row measures
-    what the pageable tier costs against the all-pinned headline."""
+    from the pageable home before the DMA — on a pool of copy workers,
+    staged several layers ahead of the layer being fetched
+    (HostTier::stage) — so this row measures what the pageable tier costs
+    against the all-pinned headline."""
     from paper_2410_00428_b200 import layersim as ls
     from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
     model = ls.llama2_7b()
@@ -633,6 +656,7 @@ def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=
             times.append(time.perf_counter() - t0)
     st = dev.decode_stats()
     t1s = dev.host_tier_stats()
+    slot_b = dev.slot_bytes
     bad = dev.verify_request(B - 1, ctx, SEED)
     dev.close()
     step_s = min(times)
@@ -642,9 +666,14 @@ def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=
             "step_s": step_s, "prefetch_gbs": fetch / step_s / 1e9, "link_h2d_peak_gbs": link["h2d"],
             "frac_of_link": fetch / step_s / 1e9 / link["h2d"],
             "read_in_frames_per_step": (t1s.read_in_frames - t0s.read_in_frames) / (steps + 1),
+            "read_in_gbs": (t1s.read_in_frames - t0s.read_in_frames) / (steps + 1) * slot_b / step_s / 1e9,
             "hit_rate": (t1s.hits - t0s.hits) / max(1, (t1s.hits - t0s.hits) + (t1s.misses - t0s.misses)),
+            "read_ahead_layers": t1s.read_ahead, "copy_threads": t1s.copy_threads,
+            "staged_per_step": (t1s.staged - t0s.staged) / (steps + 1),
+            "pin_waits_per_step": (t1s.pin_waits - t0s.pin_waits) / (steps + 1),
             "kv_verified_mismatches": bad,
-            "timing": "wall clock around decode_begin..synchronize (host read-ins are on the critical path)"}
+            "timing": "wall clock around decode_begin..synchronize (host read-ins included)",
+            "read_ins": "copy-worker pool, staged read_ahead_layers ahead of each layer's DMA (HostTier::stage)"}
 
 
 def scatter_gather_row(torch, dev_t, hbm_peak, T=16384, L=4):
@@ -763,18 +792,22 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    if os.environ.get("LKV_BENCH_ONE_GPU") == "1":  # code-path check only: every rank on cuda:0 (numbers meaningless)
+    one_gpu = os.environ.get("LKV_BENCH_ONE_GPU") == "1"
+    if one_gpu:  # code-path check only: every rank on cuda:0 (numbers meaningless)
         local = 0
     torch.cuda.set_device(local)
     dev_t = torch.device("cuda", local)
-    if world > 1:
-        # control plane (handle exchange, barriers, max over ranks) on gloo; NCCL only for the baseline all-gather
-        if args.allgather == "nccl":
-            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev_t)
-        else:
-            dist.init_process_group("gloo")
     from paper_2410_00428_b200 import layersim as ls
-    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig
+    from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig, bind_to_numa_node
+    numa = bind_to_numa_node(local)  # before any pinned allocation of this process
+    if world > 1:
+        # control plane (handle exchange, barriers, max over ranks) on gloo;
+        # NCCL for the baseline all-gather and for checking the fused one
+        # (NCCL cannot put two ranks on one GPU: the one-GPU check stays on gloo)
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("cpu:gloo,cuda:nccl", device_id=dev_t)
 
     model = ls.llama2_7b()
     L, bs, d = model.n_layers, 16, model.d_head
@@ -793,7 +826,7 @@ def main():
     cs = dev.torch_stream("compute")
     hbm_peak, peak_kind = peaks()
 
-    link = host_link_peak(torch, dev_t)
+    link = host_link_peak(torch, dev_t, world)
 
     # ---------------- setup: real prefill offload of every request (pack + D2H)
     k = torch.empty((ctx, hl, d), dtype=torch.bfloat16, device=dev_t)
@@ -827,7 +860,7 @@ def main():
         dist.barrier()
     dev.set_timing(True)
 
-    def step(qsrc=None, outdst=None):
+    def step(qsrc=None, outdst=None, capture=None):
         dev.decode_begin(ids)
         for layer in range(L):
             if qsrc is not None:
@@ -836,6 +869,9 @@ def main():
             dev.decode_layer(layer, q[layer], out[layer], scale, DTYPE_BF16, stream=cs)
             if fused:  # the one exchange, done by the merge kernel: wait for every rank's rows of this layer
                 dev.gather_wait(layer, stream=cs)
+                if capture is not None:  # valid until layer + 2 reuses the parity
+                    with torch.cuda.stream(cs):
+                        capture.append(dev.gathered(layer)[:B].clone())
             elif world > 1:
                 with torch.cuda.stream(cs):  # baseline: a separate NCCL all-gather of per-head outputs
                     dist.all_gather_into_tensor(gathered[layer], out[layer].reshape(-1))
@@ -847,7 +883,33 @@ def main():
     for _ in range(args.warmup):
         step()
     dev.synchronize()
+    multi = None
     if world > 1:
+        dist.barrier()
+        # first N>1 step checked: the fused gather's rows == an all-gather of
+        # every rank's own outputs (NCCL; gloo in the one-GPU check), bit for bit
+        got = []
+        step(capture=got if fused else None)
+        dev.synchronize()
+        ok = True
+        if fused:
+            from paper_2410_00428_b200 import tp
+            for layer in range(L):  # tp.all_gather_heads: the path's collective as a plain all-gather
+                want = tp.all_gather_heads(dist, out[layer].cpu() if one_gpu else out[layer])
+                ok &= bool(torch.equal(got[layer].to(want.device), want))
+        flag = torch.tensor([1 if ok else 0], dtype=torch.int64)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        place = dev.placement()
+        peers = torch.tensor([place["gather_peers_p2p"]], dtype=torch.int64)
+        dist.all_reduce(peers, op=dist.ReduceOp.MIN)
+        multi = {"allgather": "fused peer stores in the split merge" if fused else "NCCL all_gather_into_tensor",
+                 "gather_verified": bool(flag.item()) if fused else None,
+                 "gather_verified_against": ("gloo all_gather (one-GPU check)" if one_gpu else
+                                             "NCCL all_gather_into_tensor of every rank's own rows") if fused else None,
+                 "peers_connected": int(peers.item()), "peers_expected": 0 if one_gpu else world - 1,
+                 "nccl": not one_gpu, "numa": numa, "pinned_pool_numa_node": place["numa_node"]}
+        if fused and not flag.item():
+            raise RuntimeError("fused all-gather rows differ from the reference all-gather")
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -956,6 +1018,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": qbytes + h2d_phys // args.steps,
                     "d2h_bytes_per_step": qbytes},
             "gpu_launches": launches,
+            "multi_gpu": multi,
             "rows": None,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -258,8 +258,14 @@ typedef struct lkv_device_info {
   void* compute_stream; /* cudaStream_t: scatter, gather, table sync, attention */
   void* d2h_stream;     /* cudaStream_t: offload copies */
   void* h2d_stream;     /* cudaStream_t: prefetch copies */
+  int32_t numa_node;    /* NUMA node the pinned host pool was bound to (the GPU's, sysfs); -1 none */
+  int32_t gather_peers; /* gather peers on other GPUs reached over P2P (NVLink) after gather_connect */
 } lkv_device_info;
 
+/* NUMA node of CUDA device `cuda_device` (its PCI function's numa_node in
+ * sysfs; -1 when unknown or single-node). Callers pin their own host buffers
+ * there (the device does it for its pools). */
+LKV_API int lkv_device_numa_node(int32_t cuda_device, int32_t* node);
 LKV_API int lkv_device_create(const lkv_model_spec* model, int32_t tokens_per_block,
                       const lkv_device_config* cfg, lkv_device** out);
 LKV_API int lkv_device_destroy(lkv_device* dev);
@@ -421,6 +427,10 @@ LKV_API int lkv_device_read_host_slot(lkv_device* dev, int64_t cpu_slot, void* d
 LKV_API int lkv_device_free_stack(lkv_device* dev, int32_t which, uint32_t* out, int64_t cap, int64_t* size);
 typedef struct lkv_host_tier_stats {
   int64_t pinned_frames, read_in_frames, write_back_frames, evictions, hits, misses;
+  int64_t staged;           /* slots whose read-in was started ahead of their prefetch */
+  int64_t pin_waits;        /* prefetches that waited for a read-in still running */
+  int32_t read_ahead;       /* layers staged beyond the one being fetched (last decode iteration) */
+  int32_t copy_threads;     /* read-in / write-back workers */
 } lkv_host_tier_stats;
 LKV_API int lkv_device_host_tier_stats(const lkv_device* dev, lkv_host_tier_stats* out);
 /* Writes generator data for every entry of a request (GPU slots and host

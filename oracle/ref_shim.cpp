@@ -269,6 +269,33 @@ int lkv_kv_free_stack(const lkv_kv_manager* k, int32_t which, uint32_t* out, int
 }
 #endif
 
+#ifdef LKV_SHIM_HYBRID
+int lkv_kv_free_delta(lkv_kv_manager* k, int32_t which, int32_t full, int64_t* next_fresh, int64_t* low,
+                      int64_t* size, int32_t* changed, uint32_t* out, int64_t cap) {
+  TRY const auto d = k->impl.take_free_delta(which == 0, full != 0);
+  *next_fresh = d.next_fresh;
+  *low = d.low;
+  *size = d.size;
+  *changed = d.changed ? 1 : 0;
+  if (cap >= d.size - d.low) std::copy(d.pushed + d.low, d.pushed + d.size, out);
+  CATCH
+}
+#else
+// The reference keeps the whole stack explicitly: every take is a full
+// delta with no implicit fresh part (next_fresh = total).
+int lkv_kv_free_delta(lkv_kv_manager* k, int32_t which, int32_t, int64_t* next_fresh, int64_t* low, int64_t* size,
+                      int32_t* changed, uint32_t* out, int64_t cap) {
+  TRY const auto& pool = which == 0 ? k->impl.*rob(GpuPoolTag{}) : k->impl.*rob(CpuPoolTag{});
+  const std::vector<std::uint32_t>& st = pool.*rob(StackTag{});
+  *next_fresh = which == 0 ? k->impl.gpu_blocks_total() : k->impl.cpu_blocks_total();
+  *low = 0;
+  *size = static_cast<int64_t>(st.size());
+  *changed = 1;
+  if (cap >= *size) std::copy(st.begin(), st.end(), out);
+  CATCH
+}
+#endif
+
 int lkv_kv_dump_hash(const lkv_kv_manager* k, uint64_t* o) {
   TRY std::ostringstream os;
   k->impl.dump_table(os);

@@ -107,13 +107,15 @@ class DeviceConfig(C.Structure):
 
 class HostTierStats(C.Structure):
     _fields_ = [("pinned_frames", i64), ("read_in_frames", i64), ("write_back_frames", i64), ("evictions", i64),
-                ("hits", i64), ("misses", i64)]
+                ("hits", i64), ("misses", i64), ("staged", i64), ("pin_waits", i64), ("read_ahead", i32),
+                ("copy_threads", i32)]
 
 
 class DeviceInfo(C.Structure):
     _fields_ = [("slot_bytes", i64), ("kv_heads_local", i32), ("q_heads_local", i32),
                 ("head_dim", i32), ("tokens_per_block", i32), ("pool", vp), ("host_pool", vp),
-                ("arena", vp), ("compute_stream", vp), ("d2h_stream", vp), ("h2d_stream", vp)]
+                ("arena", vp), ("compute_stream", vp), ("d2h_stream", vp), ("h2d_stream", vp),
+                ("numa_node", i32), ("gather_peers", i32)]
 
 
 class DecodeStats(C.Structure):
@@ -165,6 +167,7 @@ _PROTOS = {
     "lkv_kv_dump_table": [vp, C.c_char_p, C.c_size_t, P(C.c_size_t)],
     "lkv_kv_dump_hash": [vp, P(u64)],
     "lkv_kv_free_stack": [vp, i32, P(u32), i64, P(i64)],
+    "lkv_device_numa_node": [i32, P(i32)],
     "lkv_kv_free_delta": [vp, i32, i32, P(i64), P(i64), P(i64), P(i32), P(u32), i64],
     "lkv_bus_create": [f64, P(vp)],
     "lkv_bus_destroy": [vp],

@@ -286,7 +286,8 @@ struct lkv_device final : layersim::KvObserver {
     numa_node = gpu_numa_node(cfg.device);
     const int cores = static_cast<int>(std::thread::hardware_concurrency());
     if (cfg.pinned_frames > 0 && cfg.host_slots > 0) {  // tiered: homes pageable, frames pinned
-      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb, std::clamp(cores, 2, 16), numa_node);
+      // copy workers: the cores left beside the API and cleaner threads
+      tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb, std::clamp(cores - 2, 2, 16), numa_node);
       host_pool = tier.pinned();
       LKV_CUDA(cudaMalloc(&d_xlat, cfg.host_slots * sizeof(int)));
     } else if (cfg.host_slots > 0) {
@@ -853,6 +854,48 @@ struct lkv_device final : layersim::KvObserver {
   }
 
   // ----------------------------------------------------------------- decode
+  // Layer l's prefetch: every member's CPU-located blocks (blocks past the
+  // member's fetch length are the appended token's fresh block), their arena
+  // frames, and the token-exact bytes plan_decode_fetch books for them.
+  struct FetchPlan {
+    std::vector<long long> slots, dst;
+    std::vector<std::size_t> first;  // [members + 1] member ranges in slots / dst
+    long long tokens = 0;
+  };
+  FetchPlan fetch_plan(int l) const {
+    FetchPlan p;
+    const int st = l % cfg.pipeline_depth;
+    const long long arena0 = cfg.gpu_slots + static_cast<long long>(st) * cfg.arena_slots;
+    p.first.assign(members.size() + 1, 0);
+    for (std::size_t mi = 0; mi < members.size(); ++mi) {
+      const Member& m = members[mi];
+      const RequestKv& r = kv->request(m.id);
+      for (int b = 0; b < m.nblk; ++b) {
+        if (static_cast<long long>(b) * bs >= m.fetch_len) break;
+        const auto& e = r.blocks[b].layers[l];
+        if (e.loc != Loc::Cpu) continue;
+        check_slot(e);
+        p.slots.push_back(e.slot);
+        p.dst.push_back(arena0 + m.blk_off + b);
+        p.tokens += std::clamp<long long>(m.fetch_len - static_cast<long long>(b) * bs, 0, bs);
+      }
+      p.first[mi + 1] = p.slots.size();
+    }
+    return p;
+  }
+
+  // Tiered host memory: layers whose read-ins were started ahead of their
+  // prefetch (HostTier::stage), `read_ahead` layers beyond the one issued.
+  int read_ahead = 0;
+  std::vector<std::vector<long long>> staged_slots;  // [L] slots staged, not yet pinned
+  std::vector<char> staged;                          // [L]
+  void stage_layer(int l) {
+    if (!tiered() || l >= L || staged[l]) return;
+    staged[l] = 1;
+    staged_slots[l] = fetch_plan(l).slots;
+    if (!staged_slots[l].empty()) tier.stage(staged_slots[l].data(), static_cast<long long>(staged_slots[l].size()));
+  }
+
   void issue_fetch(int l) {
     const int st = l % cfg.pipeline_depth;
     if (attn_recorded[st]) LKV_CUDA(cudaStreamWaitEvent(h2d, attn_done[st], 0));
@@ -860,43 +903,31 @@ struct lkv_device final : layersim::KvObserver {
       LKV_CUDA(cudaEventRecord(t_h2d0, h2d));
       h2d_started = true;
     }
-    const long long arena0 = cfg.gpu_slots + static_cast<long long>(st) * cfg.arena_slots;
     const long long copies0 = dstats.h2d_copies;
     if (timing) LKV_CUDA(cudaEventRecord(t_f0[l], h2d));
-    std::vector<long long> all_slots, all_frames;
-    std::vector<std::size_t> first(members.size() + 1, 0);
-    std::vector<long long> all_dst;
-    for (std::size_t mi = 0; mi < members.size(); ++mi) {
-      const Member& m = members[mi];
-      const RequestKv& r = kv->request(m.id);
-      long long tok = 0;
-      for (int b = 0; b < m.nblk; ++b) {
-        if (static_cast<long long>(b) * bs >= m.fetch_len) break;  // the appended token's fresh block
-        const auto& e = r.blocks[b].layers[l];
-        if (e.loc != Loc::Cpu) continue;
-        check_slot(e);
-        all_slots.push_back(e.slot);
-        all_dst.push_back(arena0 + m.blk_off + b);
-        tok += std::clamp<long long>(m.fetch_len - static_cast<long long>(b) * bs, 0, bs);
-      }
-      first[mi + 1] = all_slots.size();
-      dstats.h2d_bytes_algorithmic += tok * (sb / bs);
+    FetchPlan p = fetch_plan(l);
+    dstats.h2d_bytes_algorithmic += p.tokens * (sb / bs);
+    std::vector<long long> all_frames;
+    host_frames(p.slots, true, &all_frames);  // tiered: staged read-ins landed / missing slots read in
+    if (tiered() && l < L) {
+      staged[l] = 1;  // its stage locks became the pin's locks
+      staged_slots[l].clear();
     }
-    host_frames(all_slots, true, &all_frames);  // tiered: read in missing slots from their homes
     for (std::size_t mi = 0; mi < members.size(); ++mi) {
-      const std::size_t a = first[mi], n = first[mi + 1] - a;
+      const std::size_t a = p.first[mi], n = p.first[mi + 1] - a;
       if (n == 0) continue;
-      dstats.h2d_copies += emit_copies(dbuf, all_dst.data() + a, host_pool, all_frames.data() + a,
+      dstats.h2d_copies += emit_copies(dbuf, p.dst.data() + a, host_pool, all_frames.data() + a,
                                        static_cast<long long>(n), cudaMemcpyHostToDevice, h2d);
       dstats.h2d_bytes_physical += static_cast<long long>(n) * sb;
     }
-    host_done(all_slots, h2d, false);
+    host_done(p.slots, h2d, false);
     LKV_CUDA(cudaEventRecord(fetch_done[st], h2d));
     if (timing) {
       LKV_CUDA(cudaEventRecord(t_f1[l], h2d));
       fetched[l] = dstats.h2d_copies > copies0;
       LKV_CUDA(cudaEventRecord(t_h2d1, h2d));
     }
+    stage_layer(l + read_ahead);  // keep the read-ins `read_ahead` layers ahead of the DMA
   }
 
   void decode_begin(const int64_t* ids, int n, bool append = false) {
@@ -959,6 +990,17 @@ struct lkv_device final : layersim::KvObserver {
       LKV_CUDA(cudaMemsetAsync(d_stamps, 0, static_cast<std::size_t>(std::max(L, 1)) * 16, cs));
     }
     in_iteration = true;
+    if (tiered()) {
+      // read-ahead depth: as many layers as the pinned frames hold beside the
+      // ones the prefetch pipeline has in flight (and one draining)
+      long long per_layer = 0;
+      for (const Member& m : members) per_layer += m.nblk;
+      const long long fit = per_layer > 0 ? cfg.pinned_frames / per_layer : L;
+      read_ahead = static_cast<int>(std::clamp<long long>(fit - cfg.pipeline_depth - 1, 0, L));
+      staged.assign(L, 0);
+      staged_slots.assign(L, {});
+      for (int l = 0; l < std::min(read_ahead + cfg.pipeline_depth, L); ++l) stage_layer(l);
+    }
     for (int l = 0; l < std::min(cfg.pipeline_depth, L); ++l) issue_fetch(l);
   }
 
@@ -1157,10 +1199,33 @@ struct lkv_device final : layersim::KvObserver {
     return d_gather;
   }
 
+  int gather_peers = 0;  // peers on other devices (P2P over NVLink)
   void gather_connect(const std::vector<char*>& bases) {
     if (static_cast<int>(bases.size()) != cfg.tp_size) throw std::invalid_argument("gather: need one base per rank");
     if (cfg.tp_size > kGatherFlagWords) throw std::invalid_argument("gather: too many ranks");
     if (bases[cfg.tp_rank] != gather_buffer()) throw std::invalid_argument("gather: own slot must be own buffer");
+    // Peers' buffers on other GPUs: the merge kernel stores into them and the
+    // wait kernel polls its own, so this device needs peer access to each
+    // (IPC mappings enable it lazily; same-process peers need it explicitly).
+    gather_peers = 0;
+    for (int r = 0; r < cfg.tp_size; ++r) {
+      if (r == cfg.tp_rank) continue;
+      cudaPointerAttributes a{};
+      LKV_CUDA(cudaPointerGetAttributes(&a, bases[r]));
+      if (a.type != cudaMemoryTypeDevice) throw std::invalid_argument("gather: peer base is not device memory");
+      if (a.device == cfg.device) continue;
+      int can = 0;
+      LKV_CUDA(cudaDeviceCanAccessPeer(&can, cfg.device, a.device));
+      if (!can)
+        throw CudaError("gather: device " + std::to_string(cfg.device) + " cannot access peer device " +
+                        std::to_string(a.device) + " (no P2P path)");
+      const cudaError_t e = cudaDeviceEnablePeerAccess(a.device, 0);
+      if (e == cudaErrorPeerAccessAlreadyEnabled)
+        cudaGetLastError();
+      else
+        LKV_CUDA(e);
+      ++gather_peers;
+    }
     gather_bases = bases;
     if (!d_gather_bases) LKV_CUDA(cudaMalloc(&d_gather_bases, kGatherFlagWords * sizeof(char*)));
     if (!d_gather_done) LKV_CUDA(cudaMalloc(&d_gather_done, sizeof(unsigned)));
@@ -1238,6 +1303,12 @@ struct lkv_device final : layersim::KvObserver {
   void decode_end() {
     if (!in_iteration) throw layersim::SimulationError("decode_end without decode_begin");
     in_iteration = false;
+    if (tiered())  // layers staged but never fetched (an iteration cut short) give their frames back
+      for (auto& s : staged_slots)
+        if (!s.empty()) {
+          tier.unstage(s.data(), static_cast<long long>(s.size()));
+          s.clear();
+        }
     if (timing) {
       LKV_CUDA(cudaStreamWaitEvent(cs, fetch_done[(L - 1) % cfg.pipeline_depth], 0));
       LKV_CUDA(cudaEventRecord(t_it1, cs));
@@ -1295,6 +1366,12 @@ int lkv_device_create(const lkv_model_spec* m, int32_t tpb, const lkv_device_con
   return LKV_OK;
 }
 
+int lkv_device_numa_node(int32_t cuda_device, int32_t* node) {
+  LKV_REQUIRE(node && cuda_device >= 0);
+  *node = lkv::gpu_numa_node(cuda_device);
+  return LKV_OK;
+}
+
 int lkv_device_destroy(lkv_device* d) {
   delete d;
   return LKV_OK;
@@ -1313,6 +1390,8 @@ int lkv_device_get_info(const lkv_device* d, lkv_device_info* o) {
   o->compute_stream = d->cs;
   o->d2h_stream = d->d2h;
   o->h2d_stream = d->h2d;
+  o->numa_node = d->tiered() ? d->tier.numa_node() : d->host_mem.node();
+  o->gather_peers = d->gather_peers;
   return LKV_OK;
 }
 
@@ -1710,6 +1789,10 @@ int lkv_device_host_tier_stats(const lkv_device* d, lkv_host_tier_stats* o) {
     o->evictions = t.evictions;
     o->hits = t.hits;
     o->misses = t.misses;
+    o->staged = t.staged;
+    o->pin_waits = t.pin_waits;
+    o->read_ahead = d->read_ahead;
+    o->copy_threads = d->tier.copy_threads();
   }
   return LKV_OK;
 }

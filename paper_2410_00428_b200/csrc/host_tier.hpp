@@ -119,6 +119,7 @@ class HostTier {
   char* pinned() const { return pinned_; }
   long long frames() const { return F_; }
   int numa_node() const { return pinned_mem_.node(); }
+  int copy_threads() const { return threads_; }
   HostTierStats stats() const {
     std::lock_guard<std::mutex> g(mu_);
     return st_;
@@ -179,10 +180,10 @@ class HostTier {
     // a staged read-in still running must land before the caller reads the
     // frame, or before a GPU write replaces it (else it would overwrite it)
     g.lock();
+    long long i0 = 0;  // frames before i0 have landed (resumes after each wake-up)
     auto filling = [&] {
-      for (long long i = 0; i < n; ++i)
-        if (frames_[static_cast<std::size_t>(frames_out[i])].filling) return true;
-      return false;
+      while (i0 < n && !frames_[static_cast<std::size_t>(frames_out[i0])].filling) ++i0;
+      return i0 < n;
     };
     if (filling()) {
       ++st_.pin_waits;

@@ -73,6 +73,38 @@ def _device_view(ptr: int, shape, dtype, device: int):
         return torch.as_tensor(_Arr(), device=torch.device("cuda", device)).view(dtype)
 
 
+def numa_node(cuda_device: int) -> int:
+    """NUMA node of a CUDA device (include/lkv.h lkv_device_numa_node); -1
+    when unknown or single-node."""
+    n = C.c_int32()
+    _abi.product_lib().call("lkv_device_numa_node", cuda_device, C.byref(n))
+    return n.value
+
+
+def bind_to_numa_node(cuda_device: int) -> dict:
+    """Pin this process's threads to the CPUs of the GPU's NUMA node, so host
+    buffers it allocates (first touch) and the copy threads sit next to the
+    GPU's PCIe link. No-op on single-node hosts."""
+    import os
+    node = numa_node(cuda_device)
+    nodes = [d for d in os.listdir("/sys/devices/system/node") if d.startswith("node")] \
+        if os.path.isdir("/sys/devices/system/node") else []
+    out = {"numa_node": node, "numa_nodes": len(nodes), "cpus": None}
+    if node < 0 or len(nodes) < 2:
+        return out
+    try:
+        with open(f"/sys/devices/system/node/node{node}/cpulist") as f:
+            cpus = set()
+            for part in f.read().strip().split(","):
+                lo, _, hi = part.partition("-")
+                cpus.update(range(int(lo), int(hi or lo) + 1))
+        os.sched_setaffinity(0, cpus)
+        out["cpus"] = len(cpus)
+    except OSError:
+        pass
+    return out
+
+
 class Device:
     """One GPU's KV-head shard of the LayerKV data path, bound to a KvManager."""
 
@@ -183,6 +215,14 @@ class Device:
         """Same-process ranks: connect with each rank's gather_buffer() pointer."""
         arr = (C.c_void_p * len(bases))(*bases)
         self._lib.call("lkv_device_gather_connect", self.handle, arr, len(bases))
+
+    def placement(self) -> dict:
+        """Where this rank's resources sit: the NUMA node its pinned host pool
+        was bound to (-1: none / single node) and how many gather peers on
+        other GPUs it reaches over P2P (after gather_connect*)."""
+        info = _abi.DeviceInfo()
+        self._lib.call("lkv_device_get_info", self.handle, C.byref(info))
+        return {"numa_node": info.numa_node, "gather_peers_p2p": info.gather_peers}
 
     def gather_wait(self, layer: int, stream=None):
         """Enqueue on `stream` a wait for every rank's rows of `layer`."""

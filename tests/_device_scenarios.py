@@ -24,12 +24,12 @@ def gqa_model(L=4, hkv=8, group=4, d=128):
 
 
 def make(model, bs=16, gpu=512, cpu=512, tp_rank=0, tp_size=1, depth=2, chunk_slots=3, max_blocks=64,
-         max_batch=8, arena=None, pinned=0):
+         max_batch=8, arena=None, pinned=0, device=0):
     """pinned > 0: tiered host memory (pageable homes for all `cpu` slots,
     `pinned` pinned frames)."""
     kv = ls.KvManager(ls.BlockPools(gpu, cpu, bs), model)
     slot_bytes = 2 * (model.n_kv_heads // tp_size) * bs * model.d_head * 2
-    cfg = DeviceConfig(device=0, tp_rank=tp_rank, tp_size=tp_size, pipeline_depth=depth, gpu_slots=gpu,
+    cfg = DeviceConfig(device=device, tp_rank=tp_rank, tp_size=tp_size, pipeline_depth=depth, gpu_slots=gpu,
                        host_slots=cpu, arena_slots=arena or gpu, max_requests=16, max_blocks=max_blocks,
                        max_batch=max_batch, staging_chunks=4, chunk_bytes=chunk_slots * slot_bytes,
                        pinned_frames=pinned)
@@ -42,7 +42,8 @@ def prefill(kv, dev, rid, prompt, x, seed=SEED):
     import torch
     assert kv.allocate_prefill(rid, prompt, x)
     L = dev.model.n_layers
-    k = torch.empty((prompt, dev.kv_heads_local, dev.head_dim), dtype=torch.bfloat16, device="cuda:0")
+    k = torch.empty((prompt, dev.kv_heads_local, dev.head_dim), dtype=torch.bfloat16,
+                    device=f"cuda:{dev.cfg.device}")
     v = torch.empty_like(k)
     s = dev.torch_stream("compute")
     for layer in range(L):
@@ -96,6 +97,14 @@ def peaked_q(dev, layer, kv_lens, mode, seed=SEED, gen_seed=0):
     return torch.from_numpy(q).to(torch.bfloat16)
 
 
+def rel_err_rows(got, want):
+    """Per-row relative error max|got - want| / max|want|, with a non-finite
+    output row counted as +inf (NaN compares false: max(worst, nan) and
+    nan > tol would otherwise let a NaN row pass)."""
+    err = np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)
+    return np.where(np.isfinite(err) & np.isfinite(got).all(axis=-1), err, np.inf)
+
+
 def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=None, tol=None, q_mode=None):
     """One decode iteration over `ids`; every layer compared with the oracle.
     q_mode: None = U(-1, 1) queries; "scaled" / "rising" = peaked_q."""
@@ -127,7 +136,7 @@ def check_attention(dev, ids, kv_lens, seed=SEED, out_dtype=DTYPE_F32, layers=No
         q16 = qs[l].view(torch.int16).numpy().view(np.uint16)
         for m in range(n):
             want = re.decode_attn_gen(seed, l, kv_lens[m], dev.head0, dev.kv_heads_local, group, q16[m], scale)
-            err = np.abs(got[m] - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)
+            err = rel_err_rows(got[m], want)
             worst = max(worst, float(err.max()))
             if err.max() > limit:
                 h = int(np.argmax(err))
@@ -185,6 +194,6 @@ def check_prefill_attention(dev, T, seed=SEED):
                            k.cpu().view(torch.int16).numpy().view(np.uint16),
                            v.cpu().view(torch.int16).numpy().view(np.uint16), 1.0 / math.sqrt(d))
     got = out.cpu().numpy()
-    err = float((np.abs(got - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)).max())
+    err = float(rel_err_rows(got, want).max())
     assert err <= REL_TOL, f"prefill attention rel err {err:.3e} > {REL_TOL}"
     return err

@@ -62,8 +62,7 @@ def _decode_step(kv, dev, ids, check=True):
             for m in range(len(ids)):
                 want = re.decode_attn_gen(sc.SEED, l, lens[m], dev.head0, dev.kv_heads_local, group, q16[m],
                                           1 / math.sqrt(d))
-                err = np.abs(got[m] - want).max(axis=-1) / np.maximum(np.abs(want).max(axis=-1), 1e-30)
-                worst = max(worst, float(err.max()))
+                worst = max(worst, float(sc.rel_err_rows(got[m], want).max()))
         assert worst <= sc.REL_TOL, f"attention rel err {worst:.3e}"
     for rid in ids:  # engine.cpp:151
         kv.note_token(rid)

@@ -297,3 +297,17 @@ def test_free_delta_journal_replays_the_stacks():
         return check
     drv.fuzz_ops(None, seed=31, rounds=3, steps=300, on_kv=bind)
     assert len(mirrors) == 3 * 301
+
+
+def test_rel_err_rows_counts_nan_as_failure():
+    """The attention parity checks' error metric: a NaN or inf output row is
+    an infinite error (max() and > both ignore NaN otherwise)."""
+    import numpy as np
+    from tests import _device_scenarios as sc
+    want = np.ones((3, 4), np.float32)
+    got = want.copy()
+    assert sc.rel_err_rows(got, want).max() == 0.0
+    got[1, 2] = np.nan
+    assert np.isinf(sc.rel_err_rows(got, want)[1])
+    got[1, 2] = np.inf
+    assert np.isinf(sc.rel_err_rows(got, want).max())
