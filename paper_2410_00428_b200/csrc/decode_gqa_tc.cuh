@@ -307,6 +307,7 @@ __global__ void __launch_bounds__(224, 1) decode_gqa_tc_kernel(
         float o[16];
         tc::tmem_ld16(tl + 32 + ob * 16, o);
         tc::tmem_wait_ld();
+        tc::reg_fence<16>(o);
         tc::fence_before_sync();
         tc::bar_arrive(&o_empty[ob]);
 #pragma unroll
@@ -319,6 +320,7 @@ __global__ void __launch_bounds__(224, 1) decode_gqa_tc_kernel(
         float s[8];
         tc::tmem_ld8(tl + sb * 16, s);
         tc::tmem_wait_ld();
+        tc::reg_fence<8>(s);
         tc::fence_before_sync();
         tc::bar_arrive(&s_empty[sb]);
         const int bi = t * TB + r / BS;

@@ -40,6 +40,12 @@ using layersim::OffloadEntry;
 using layersim::OffloadJob;
 using layersim::RequestKv;
 
+// Build-time choice of the prefill softmax's polynomial share (prefill_attn2.cuh
+// POLY; scripts/build_variant.sh builds the alternatives for A/B runs).
+#ifndef LKV_PREFILL_POLY
+#define LKV_PREFILL_POLY 0
+#endif
+
 namespace lkv {
 
 #define LKV_CUDA(expr)                                                                   \
@@ -1457,11 +1463,18 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   const int chunk_kv = static_cast<int>(std::clamp<long long>(kL2Budget / std::max(kv_per_head, 1ll), 1, d->Hl));
   const int chunk_q = chunk_kv * d->G;
   const long long npairs_all = (nq_all + 1) / 2;
-  auto fn2 = prefill_attn2_kernel<0>;
+  auto fn2 = prefill_attn2_kernel<LKV_PREFILL_POLY>;
   d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
   cudaLaunchConfig_t lc{};
-  lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));
-  lc.blockDim = dim3(320);
+  // persistent: one CTA per SM walks the items (query head, tile pair) in
+  // dispatch order; the next item's Q load and S MMAs overlap this one's epilogue
+  const long long items = npairs_all * d->Hql;
+#ifdef LKV_PREFILL_GRID_ALL
+  lc.gridDim = dim3(static_cast<unsigned>(items));
+#else
+  lc.gridDim = dim3(static_cast<unsigned>(std::min<long long>(items, d->sms)));
+#endif
+  lc.blockDim = dim3(kPrefillThreads);
   lc.dynamicSmemBytes = PrefillAttn2Smem::kBytes;
   lc.stream = s;
   cudaLaunchAttribute at[1];

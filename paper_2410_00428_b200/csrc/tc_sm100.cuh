@@ -175,6 +175,16 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const float* v) {
       : "memory");
 }
 
+// Ties N registers written by an asynchronous tcgen05.ld to the preceding
+// tcgen05.wait::ld: the load's outputs exist for the compiler at the ld, so
+// without this their consumers could be scheduled above the wait (volatile
+// asm statements keep their relative order).
+template <int N>
+__device__ __forceinline__ void reg_fence(float* v) {
+#pragma unroll
+  for (int i = 0; i < N; ++i) asm volatile("" : "+f"(v[i])::"memory");
+}
+
 // ---------------------------------------------------------------- UMMA
 constexpr uint32_t kLayoutNone = 0;
 constexpr uint32_t kLayoutSw128 = 2;

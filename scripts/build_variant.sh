@@ -1,0 +1,10 @@
+#!/bin/bash
+# Build an experimental variant of liblkv.so (build-time defines only; the
+# shipped library has no runtime switches) into build/variants/<name>/.
+#   bash scripts/build_variant.sh <name> "-DLKV_PREFILL_POLY=1"
+set -e
+ROOT=$(cd "$(dirname "$0")/.." && pwd)
+NAME=$1; DEFS=$2
+make -s -C "$ROOT/paper_2410_00428_b200" -j8 BUILD="$ROOT/build/variants/$NAME/obj" \
+  LIB="$ROOT/build/variants/$NAME/liblkv.so" EXTRA_NVFLAGS="$DEFS"
+echo "$ROOT/build/variants/$NAME/liblkv.so"

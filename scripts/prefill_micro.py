@@ -27,11 +27,15 @@ def main():
     p.add_argument("--hq", type=int, default=32)
     p.add_argument("--hkv", type=int, default=8)
     p.add_argument("--iters", type=int, default=5)
+    p.add_argument("--lib", default=None, help="an alternative liblkv.so (scripts/build_variant.sh)")
+    p.add_argument("--label", default="product")
     a = p.parse_args()
+    from paper_2410_00428_b200 import _abi
+    lib = _abi.Lib(a.lib) if a.lib else None
     model = ls.ModelSpec(1, a.hq, a.hkv, 128, a.hq * 128, 8e9, 2)
-    kv = ls.KvManager(ls.BlockPools(64, 64, 16), model)
+    kv = ls.KvManager(ls.BlockPools(64, 64, 16), model, lib=lib)
     dev = Device(kv, model, 16, DeviceConfig(gpu_slots=64, host_slots=64, arena_slots=64, max_requests=2,
-                                             max_blocks=64, max_batch=2))
+                                             max_blocks=64, max_batch=2), lib=lib)
     T = a.tokens
     q = (torch.rand((T, a.hq, 128), device="cuda") * 2 - 1).to(torch.bfloat16)
     k = (torch.rand((T, a.hkv, 128), device="cuda") * 2 - 1).to(torch.bfloat16)
@@ -50,7 +54,7 @@ def main():
             times.append(e0.elapsed_time(e1))
     ms = min(times)
     flops = 4.0 * 128 * a.hq * T * (T + 1) / 2
-    print(json.dumps({"tokens": T, "hq": a.hq, "hkv": a.hkv, "ms": ms, "tflops": flops / ms / 1e9,
+    print(json.dumps({"lib": a.label, "tokens": T, "hq": a.hq, "hkv": a.hkv, "ms": ms, "tflops": flops / ms / 1e9,
                       "frac_of_1624.4": flops / ms / 1e9 / 1624.4}))
     dev.close()
 
