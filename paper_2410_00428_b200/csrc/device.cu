@@ -625,24 +625,15 @@ struct lkv_device final : layersim::KvObserver {
     return copies;
   }
 
-  // Linear copies of one emit_copies call: a single cudaMemcpyBatchAsync when
-  // there are several (scattered frames, e.g. tiered host frames), instead of
-  // one API call per frame.
+  // Linear copies of one emit_copies call, one cudaMemcpyAsync each (the
+  // batched-copy API is closed on this pool: it raised GPU faults). Tiered
+  // frames are handed out in ascending order, so runs coalesce before this.
   std::vector<void*> b_dst, b_src;
   std::vector<std::size_t> b_size;
   int flush_linear(cudaMemcpyKind kind, cudaStream_t s) {
     const std::size_t n = b_dst.size();
-    int copies = 0;
-    if (n == 1 || (n > 1 && s == nullptr)) {
-      for (std::size_t k = 0; k < n; ++k) LKV_CUDA(cudaMemcpyAsync(b_dst[k], b_src[k], b_size[k], kind, s));
-      copies = static_cast<int>(n);
-    } else if (n > 1) {
-      cudaMemcpyAttributes attr{};
-      attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-      std::size_t idx0 = 0, fail = 0;
-      LKV_CUDA(cudaMemcpyBatchAsync(b_dst.data(), b_src.data(), b_size.data(), n, &attr, &idx0, 1, &fail, s));
-      copies = 1;
-    }
+    for (std::size_t k = 0; k < n; ++k) LKV_CUDA(cudaMemcpyAsync(b_dst[k], b_src[k], b_size[k], kind, s));
+    const int copies = static_cast<int>(n);
     b_dst.clear();
     b_src.clear();
     b_size.clear();
