@@ -782,6 +782,14 @@ def serving_row(link, tf_peak, hbm_peak, n=6, prompt=16384, output=8, rate=8.0):
 
 
 # ------------------------------------------------------------------ product arm
+_T0 = time.perf_counter()
+
+
+def log(msg):
+    """Progress on stderr (the JSON line is the only stdout output)."""
+    print(f"[bench {time.perf_counter() - _T0:7.1f} s] {msg}", file=sys.stderr, flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -829,6 +837,7 @@ def main():
     link = host_link_peak(torch, dev_t, world)
 
     # ---------------- setup: real prefill offload of every request (pack + D2H)
+    log("setup: prefill offload of every request")
     k = torch.empty((ctx, hl, d), dtype=torch.bfloat16, device=dev_t)
     v = torch.empty_like(k)
     dev.offload_stats(reset=True)
@@ -847,6 +856,7 @@ def main():
     bad = dev.verify_request(B - 1, ctx, SEED)
 
     # ---------------- decode iteration
+    log("decode iterations (warm-up, timed)")
     scale = 1.0 / math.sqrt(d)
     q = [torch.randn((B, hql, d), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
     out = [torch.empty((B, hql, d), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
@@ -943,6 +953,7 @@ def main():
     value = total_kv * args.steps / (elapsed / 1000) / 1e9
 
     # ---------------- e2e through the C ABI with host buffers
+    log("e2e through the C ABI")
     q_host = [t.cpu().pin_memory() for t in q]
     out_host = [torch.empty((B, hql, d), dtype=torch.bfloat16, pin_memory=True) for _ in range(L)]
     step(q_host, out_host)
@@ -1049,7 +1060,9 @@ def main():
                 if want is not None and name not in want:
                     continue
                 t0 = time.perf_counter()
+                log(f"row {name} ...")
                 r = fn()
+                log(f"row {name} done in {time.perf_counter() - t0:.1f} s")
                 if name == "prefill":
                     rows.update(r)
                 else:

@@ -1457,15 +1457,8 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   auto fn2 = prefill_attn2_kernel<LKV_PREFILL_POLY>;
   d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
   cudaLaunchConfig_t lc{};
-  // persistent: one CTA per SM walks the items (query head, tile pair) in
-  // dispatch order; the next item's Q load and S MMAs overlap this one's epilogue
-  const long long items = npairs_all * d->Hql;
-#ifdef LKV_PREFILL_GRID_ALL
-  lc.gridDim = dim3(static_cast<unsigned>(items));
-#else
-  lc.gridDim = dim3(static_cast<unsigned>(std::min<long long>(items, d->sms)));
-#endif
-  lc.blockDim = dim3(kPrefillThreads);
+  lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));
+  lc.blockDim = dim3(320);
   lc.dynamicSmemBytes = PrefillAttn2Smem::kBytes;
   lc.stream = s;
   cudaLaunchAttribute at[1];

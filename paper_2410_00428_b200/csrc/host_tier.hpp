@@ -133,11 +133,8 @@ class HostTier {
     {
       std::unique_lock<std::mutex> g(mu_);
       for (long long i = 0; i < n; ++i) {
-        bool fill = false;
-        const int f = resident_or_take(g, slots[i], &fill);
-        Frame& fr = frames_[static_cast<std::size_t>(f)];
-        fr.stage_locks += 1;
-        if (fill) jobs.push_back(fill_job(f));
+        const int f = resident_or_take(g, slots[i], jobs);
+        frames_[static_cast<std::size_t>(f)].stage_locks += 1;
       }
       st_.staged += n;
     }
@@ -167,12 +164,10 @@ class HostTier {
       if (s < 0 || s >= S_) throw std::out_of_range("host tier: CPU slot " + std::to_string(s));
       const int f0 = slot_frame_[static_cast<std::size_t>(s)];
       const bool staged = f0 >= 0 && frames_[static_cast<std::size_t>(f0)].stage_locks > 0;  // counted by stage()
-      bool fill = false;
-      const int f = resident_or_take(g, s, &fill, read, !staged);
+      const int f = resident_or_take(g, s, jobs, read, !staged);
       Frame& fr = frames_[static_cast<std::size_t>(f)];
       if (fr.stage_locks > 0) fr.stage_locks -= 1;
       fr.locks += 1;
-      if (fill) jobs.push_back(fill_job(f));
       frames_out[i] = f;
     }
     g.unlock();
@@ -277,29 +272,28 @@ class HostTier {
     return {pinned_ + f * sb_, home_ + fr.slot * sb_, f};
   }
 
-  // The slot's frame, making it resident (a fresh frame) when needed; *fill
-  // = a read-in must be started (read and the slot holds bytes). Called
-  // with mu_ held.
-  int resident_or_take(std::unique_lock<std::mutex>& g, long long s, bool* fill, bool read = true,
+  // The slot's frame, making it resident (a fresh frame) when needed; a
+  // read-in job is appended to `jobs` when the slot holds bytes and `read`.
+  // Called with mu_ held.
+  int resident_or_take(std::unique_lock<std::mutex>& g, long long s, std::vector<Job>& jobs, bool read = true,
                        bool count = true) {
     if (s < 0 || s >= S_) throw std::out_of_range("host tier: CPU slot " + std::to_string(s));
     int f = slot_frame_[static_cast<std::size_t>(s)];
     if (f >= 0) {
       if (count) ++st_.hits;
       touch(f);
-      *fill = false;
       return f;
     }
     if (count) ++st_.misses;
-    f = take_frame(g);
+    f = take_frame(g, jobs);
     Frame& fr = frames_[static_cast<std::size_t>(f)];
     fr.slot = s;
     slot_frame_[static_cast<std::size_t>(s)] = f;
     lru_.push_back(f);
     fr.pos = std::prev(lru_.end());
     fr.in_lru = true;
-    *fill = read && slot_valid_[static_cast<std::size_t>(s)];
-    fr.filling = *fill;
+    fr.filling = read && slot_valid_[static_cast<std::size_t>(s)];
+    if (fr.filling) jobs.push_back(fill_job(f));
     return f;
   }
 
@@ -332,7 +326,9 @@ class HostTier {
 
   // A free frame, evicting the least recently used evictable one (its GPU
   // use completed; written home first when dirty). Called with mu_ held.
-  int take_frame(std::unique_lock<std::mutex>& g) {
+  // `pending`: read-ins the caller has not submitted yet; they are started
+  // before this waits, since the frames they fill may be what it waits for.
+  int take_frame(std::unique_lock<std::mutex>& g, std::vector<Job>& pending) {
     for (;;) {
       if (!free_.empty()) {  // a freed frame may still be read by an in-flight copy
         const int f = free_.back();
@@ -354,6 +350,10 @@ class HostTier {
           break;
         }
       if (victim < 0) {
+        if (!pending.empty()) {
+          submit(pending);
+          pending.clear();
+        }
         bool busy = false;  // something that will make a frame evictable without this thread
         for (int f : lru_) {
           const Frame& fr = frames_[static_cast<std::size_t>(f)];

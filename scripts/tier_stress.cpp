@@ -17,6 +17,7 @@
 #include <functional>
 #include <random>
 #include <thread>
+#include <string>
 #include <vector>
 
 #include "host_tier.hpp"
@@ -70,7 +71,39 @@ std::uint64_t word(long long slot, unsigned version, long long i) {
 
 }  // namespace
 
-int main() {
+// A pin() wider than the pinned pool, over slots that hold bytes, must fail
+// loudly: the read-ins it has not submitted yet fill the only frames it could
+// wait for (the round-2 read-ahead rework deadlocked here instead).
+int too_small() {
+  int rc = 0;
+  for (int staged = 0; staged < 2; ++staged) {
+    auto* tier = new lkv::HostTier;  // leaked: its frames stay locked by the failed call
+    tier->init(0, 64, 4, kSb, 2, -1);
+    std::vector<long long> s(40), fr(40);
+    for (int i = 0; i < 40; ++i) s[static_cast<std::size_t>(i)] = i;
+    for (int i = 0; i < 40; i += 4) {  // give every slot bytes (written home through the tier)
+      tier->pin(s.data() + i, 4, false, fr.data());
+      cudaEvent_t ev = stub_event_new();
+      stub_event_complete(ev);
+      tier->used(s.data() + i, 4, ev, true);
+    }
+    try {
+      if (staged)
+        tier->stage(s.data(), 40);
+      else
+        tier->pin(s.data(), 40, true, fr.data());
+      std::printf("too small (%s): no error\n", staged ? "stage" : "pin");
+      rc = 1;
+    } catch (const std::length_error& e) {
+      std::printf("too small (%s): %s\n", staged ? "stage" : "pin", e.what());
+    }
+  }
+  std::fflush(stdout);
+  std::_Exit(rc);  // no orderly teardown of the leaked tiers
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1 && std::string(argv[1]) == "small") return too_small();
   lkv::HostTier tier;
   tier.init(0, kSlots, kFrames, kSb, 6, -1);
   Engine eng;

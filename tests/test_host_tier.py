@@ -85,3 +85,4 @@ def test_tiered_pinned_pool_too_small_is_loud():
         sc.prefill(kv, dev, 0, 16 * 40, 0)
         sc.check_attention(dev, [0], [16 * 40])  # one layer's prefetch needs 40 frames at once
     dev.close()
+
