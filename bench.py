@@ -792,6 +792,9 @@ def log(msg):
 
 def main():
     args = parse()
+    if os.environ.get("LKV_BENCH_STACKS"):  # debugging aid: Python stacks to stderr every N s
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["LKV_BENCH_STACKS"]), repeat=True, file=sys.stderr)
     if args.impl == "reference":
         reference_arm(args)
         return
@@ -987,8 +990,10 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        log("cpu_baseline leg (oracle CPU port)")
         from oracle import ref_arm  # the checker / CPU baseline only, after the timed region
-        slots = [[kv.request(rid).blocks[b].layers[l].slot for b in range(nblk)] for rid in ids for l in range(L)]
+        reqs = [kv.request(rid) for rid in ids]  # one snapshot per request (each call copies the whole table row)
+        slots = [[r.blocks[b].layers[l].slot for b in range(nblk)] for r in reqs for l in range(L)]
         port = ref_arm.Port(nblk, dev.slot_bytes, ctx, hl, hql // hl, bs, d)
         gbs, done, dt = port.timed(dev.info.host_pool, slots, args.cpu_seconds)
         cpu = {"value": gbs, "unit": "GB/s", "cores": port.threads, "kind": "port",
