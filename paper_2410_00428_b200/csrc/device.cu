@@ -142,6 +142,7 @@ struct lkv_device final : layersim::KvObserver {
   // ---- tiered host memory: pageable homes + pinned frames
   HostTier tier;
   int* d_xlat = nullptr;        // [host_slots] CPU slot -> pinned frame (verify/fill kernels)
+  FramePair* d_pull = nullptr;  // [arena_slots] (host frame, arena frame) list of one tiered prefetch
   bool tiered() const { return tier.enabled(); }
   // Frames of CPU slots for device access (identity when not tiered);
   // host_done() must follow once the work using them is enqueued on `st`.
@@ -296,6 +297,7 @@ struct lkv_device final : layersim::KvObserver {
       tier.init(cfg.device, cfg.host_slots, cfg.pinned_frames, sb, std::clamp(cores - 2, 2, 16), numa_node);
       host_pool = tier.pinned();
       LKV_CUDA(cudaMalloc(&d_xlat, cfg.host_slots * sizeof(int)));
+      LKV_CUDA(cudaMalloc(&d_pull, std::max<long long>(cfg.arena_slots, 1) * sizeof(FramePair)));
     } else if (cfg.host_slots > 0) {
       host_mem.allocate(static_cast<std::size_t>(cfg.host_slots * sb), numa_node, std::clamp(cores, 1, 32));
       host_pool = host_mem.data();
@@ -406,6 +408,7 @@ struct lkv_device final : layersim::KvObserver {
     host_mem.release();
     tier.destroy();
     cudaFree(d_xlat);
+    cudaFree(d_pull);
     cudaFree(d_table);
     cudaFree(d_free_gpu);
     cudaFree(d_free_cpu);
@@ -910,12 +913,31 @@ struct lkv_device final : layersim::KvObserver {
       staged[l] = 1;  // its stage locks became the pin's locks
       staged_slots[l].clear();
     }
-    for (std::size_t mi = 0; mi < members.size(); ++mi) {
-      const std::size_t a = p.first[mi], n = p.first[mi + 1] - a;
-      if (n == 0) continue;
-      dstats.h2d_copies += emit_copies(dbuf, p.dst.data() + a, host_pool, all_frames.data() + a,
-                                       static_cast<long long>(n), cudaMemcpyHostToDevice, h2d);
-      dstats.h2d_bytes_physical += static_cast<long long>(n) * sb;
+    if (tiered()) {
+      // the tier's frames of a layer are scattered (LRU order): one pull
+      // kernel over the link instead of one copy-engine transfer per frame
+      const long long n = static_cast<long long>(all_frames.size());
+      if (n > 0) {
+        auto* pairs = reinterpret_cast<FramePair*>(ring.reserve(n * sizeof(FramePair)));
+        for (long long i = 0; i < n; ++i) pairs[i] = {all_frames[i], p.dst[i]};
+        LKV_CUDA(cudaMemcpyAsync(d_pull, pairs, n * sizeof(FramePair), cudaMemcpyHostToDevice, h2d));
+        ring.commit(h2d);
+        const long long rounds = n * ((sb / 16 + 2047) / 2048);
+        const int grid = static_cast<int>(std::min<long long>(rounds, std::max(sms / 2, 1)));
+        pull_frames_kernel<<<grid, 256, 0, h2d>>>(host_pool, dbuf, d_pull, static_cast<int>(n), sb);
+        LKV_CUDA(cudaGetLastError());
+        dstats.kernel_launches += 1;
+        dstats.h2d_copies += 1;
+        dstats.h2d_bytes_physical += n * sb;
+      }
+    } else {
+      for (std::size_t mi = 0; mi < members.size(); ++mi) {
+        const std::size_t a = p.first[mi], n = p.first[mi + 1] - a;
+        if (n == 0) continue;
+        dstats.h2d_copies += emit_copies(dbuf, p.dst.data() + a, host_pool, all_frames.data() + a,
+                                         static_cast<long long>(n), cudaMemcpyHostToDevice, h2d);
+        dstats.h2d_bytes_physical += static_cast<long long>(n) * sb;
+      }
     }
     host_done(p.slots, h2d, false);
     LKV_CUDA(cudaEventRecord(fetch_done[st], h2d));

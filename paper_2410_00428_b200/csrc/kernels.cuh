@@ -148,6 +148,43 @@ __global__ void __launch_bounds__(256) gather_slots_v2_kernel(const char* __rest
   }
 }
 
+// Tiered prefetch (f3): pull pinned host frames over the link into the arena
+// with SM loads, one launch per layer instead of one copy-engine transfer per
+// scattered frame (the read-in hands out frames in LRU order, so a layer's
+// frames rarely form runs). pairs[i] = {host frame, arena frame}; host frames
+// are mapped pinned memory. A persistent grid walks the frames; each thread
+// keeps 8 x 16 B loads in flight (the link's latency-bandwidth product is
+// ~100 KB, so a few dozen CTAs saturate it).
+struct FramePair {
+  long long src, dst;
+};
+
+__global__ void __launch_bounds__(256) pull_frames_kernel(const char* __restrict__ host, char* __restrict__ dev,
+                                                          const FramePair* __restrict__ pairs, int n,
+                                                          long long frame_bytes) {
+  const long long nvec = frame_bytes >> 4;
+  const int per_frame = static_cast<int>((nvec + 8 * 256 - 1) / (8 * 256));  // rounds of 32 KB per frame
+  const int total = per_frame * n;
+  for (int w = blockIdx.x; w < total; w += gridDim.x) {
+    const int f = w / per_frame, r = w - f * per_frame;
+    const FramePair fp = pairs[f];
+    const char* src = host + fp.src * frame_bytes;
+    char* out = dev + fp.dst * frame_bytes;
+    const long long j0 = static_cast<long long>(r) * 8 * 256 + threadIdx.x;
+    uint4 val[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long j = j0 + u * 256;
+      if (j < nvec) val[u] = ld_stream(src + j * 16);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const long long j = j0 + u * 256;
+      if (j < nvec) st_stream(out + j * 16, val[u]);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Decode snapshot: resolve each (member, block) of one layer's table row into
 // a physical frame of the unified [pool | arena] buffer. GPU entries keep

@@ -58,20 +58,6 @@ __device__ __forceinline__ float ex2_approx(float x) {
   return y;
 }
 
-// 2^x on the FMA/ALU pipes (x <= ~126): round-to-nearest split x = n + f
-// with the 1.5*2^23 trick, a degree-3 fit of 2^f on [-0.5, 0.5] (max relative
-// error 1.03e-4, below fp16 P's 2^-11 rounding), n added to the exponent.
-// x = -inf (masked) clamps to 2^-127 -> 0 in fp16. Takes a share of the
-// softmax exponentials off the MUFU, which bounds the softmax warpgroup.
-__device__ __forceinline__ float ex2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float t = __fadd_rn(x, 12582912.f);
-  const float f = __fsub_rn(x, __fsub_rn(t, 12582912.f));
-  const float p = fmaf(fmaf(fmaf(0.05500683f, f, 0.2422056f), f, 0.69328254f), f, 1.0f);
-  const int n = __float_as_int(t) - 0x4B400000;
-  return __int_as_float(__float_as_int(p) + (n << 23));
-}
-
 // Packed fp32x2 FMA / add (sm_100 FFMA2 / FADD2): half the issue slots of
 // the softmax's scale-subtract and row-sum.
 __device__ __forceinline__ unsigned long long f2pack(float a, float b) {
@@ -93,9 +79,45 @@ __device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsign
   return r;
 }
 
-// POLY: of every 4 column pairs, this many use ex2_poly (0, 1 or 2).
+// 2^x for a pair on the FMA/ALU pipes (x <= ~126): round-to-nearest split
+// x = n + f with the 1.5*2^23 trick, a degree-3 fit of 2^f on [-0.5, 0.5]
+// (max relative error 1.03e-4, below fp16 P's 2^-11 rounding), n added to
+// the exponent field. x = -inf (masked) clamps to 2^-127 -> 0 in fp16.
+// ~10 issue slots per pair, none on the MUFU: takes a share of the softmax
+// exponentials off the MUFU, which bounds the softmax warpgroup.
+__device__ __forceinline__ void ex2_poly2(float xa, float xb, float& pa, float& pb) {
+  const unsigned long long magic = f2pack(12582912.f, 12582912.f), neg_magic = f2pack(-12582912.f, -12582912.f);
+  const unsigned long long m1 = f2pack(-1.f, -1.f), one = f2pack(1.f, 1.f);
+  const unsigned long long c3 = f2pack(0.05500683f, 0.05500683f), c2 = f2pack(0.2422056f, 0.2422056f),
+                           c1 = f2pack(0.69328254f, 0.69328254f);
+  const unsigned long long x = f2pack(fmaxf(xa, -127.f), fmaxf(xb, -127.f));
+  const unsigned long long t = fadd2(x, magic);      // 1.5*2^23 + n, n = rint(x)
+  const unsigned long long r = fadd2(t, neg_magic);  // n
+  const unsigned long long f = ffma2(r, m1, x);      // x - n in [-0.5, 0.5]
+  const unsigned long long p = ffma2(ffma2(ffma2(c3, f, c2), f, c1), f, one);
+  float ta, tb, qa, qb;
+  f2unpack(t, ta, tb);
+  f2unpack(p, qa, qb);
+  // (t_bits << 23) == n << 23 mod 2^32: the magic's bits shift out
+  pa = __int_as_float(__float_as_int(qa) + (__float_as_int(ta) << 23));
+  pb = __int_as_float(__float_as_int(qb) + (__float_as_int(tb) << 23));
+}
+
+// POLY: of every 4 column pairs, this many use ex2_poly2 (0, 1 or 2).
+// Register budget: __launch_bounds__(320, 1) lets ptxas stop at 168 (it
+// spills a few bytes there); LKV_PREFILL_MAXNREG (build-time) sets it directly.
+// LKV_PREFILL_SPEC (build-time): exponentials of tiles after the first are
+// taken against the running max while S streams in from TMEM.
+#ifndef LKV_PREFILL_SPEC
+#define LKV_PREFILL_SPEC 0
+#endif
+#ifdef LKV_PREFILL_MAXNREG
+#define LKV_PREFILL_BOUNDS __maxnreg__(LKV_PREFILL_MAXNREG)
+#else
+#define LKV_PREFILL_BOUNDS __launch_bounds__(320, 1)
+#endif
 template <int POLY>
-__global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
+__global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
     float scale_log2, int chunk_q) {
@@ -247,45 +269,105 @@ __global__ void __launch_bounds__(320, 1) prefill_attn2_kernel(
     float s[128];
     for (int j = 0; j < ntt; ++j) {
       tc::bar_wait(&s_full[t], j & 1u);
+      // S(j) was issued after PV(j-1) by the same thread, so its commit
+      // implies PV(j-1) completed: this wait returns at once. It observes
+      // every o_full phase (compute-sanitizer synccheck flags a phase that
+      // completes unobserved before the barrier's next arrival).
+      if (j > 0) tc::bar_wait(&o_full[t], (j - 1) & 1u);
       tc::fence_after_sync();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tc::tmem_ld32(tl + s_col + c * 32, s + c * 32);
-      tc::tmem_wait_ld();
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tc::reg_fence<32>(s + c * 32);
-      if (j == qt) {  // diagonal tile: key j*128 + c <= row
-#pragma unroll
-        for (int c = 0; c < 128; ++c) s[c] = (c <= r) ? s[c] : -INFINITY;
-      }
-      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
-#pragma unroll
-      for (int c = 0; c < 128; ++c) mx[c & 3] = fmaxf(mx[c & 3], s[c]);
-      const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
-      float corr = 1.f;
-      bool resc = false;
-      if (mt > m_run + 8.f) {  // lazy rescale
-        corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
-        resc = j > 0;
-        m_run = mt;
-        l_run *= corr;
-      }
+      const bool diag = j == qt;
       unsigned long long ls2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
-      const unsigned long long sc2 = f2pack(scale_log2, scale_log2), nm2 = f2pack(-m_run, -m_run);
-#pragma unroll
-      for (int c = 0; c < 4; ++c) {  // P(j) -> TMEM over S(j), 32 columns at a time
+      const unsigned long long sc2 = f2pack(scale_log2, scale_log2);
+      // P of S columns [32c, 32c + 32) against the reference maximum m (log2
+      // units) -> fp16 pairs into TMEM over S columns [16c, 16c + 16) (already
+      // in registers), their fp32 sum into ls2
+      auto exps = [&](int c, float m) {
+        const unsigned long long nm2 = f2pack(-m, -m);
         uint32_t ph[16];
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           float xa, xb;
           f2unpack(ffma2(f2pack(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2), xa, xb);
-          const bool poly = (i & 3) >= 4 - POLY;
-          const float a = poly ? ex2_poly(xa) : ex2_approx(xa);
-          const float b = poly ? ex2_poly(xb) : ex2_approx(xb);
+          float a, b;
+          if ((i & 3) >= 4 - POLY) {
+            ex2_poly2(xa, xb, a, b);
+          } else {
+            a = ex2_approx(xa);
+            b = ex2_approx(xb);
+          }
           ls2[i & 1] = fadd2(ls2[i & 1], f2pack(a, b));
           const __half2 h2 = __floats2half2_rn(a, b);
           ph[i] = *reinterpret_cast<const uint32_t*>(&h2);
         }
         tc::tmem_st16(tl + s_col + c * 16, ph);
+      };
+      auto mask = [&](int c) {  // diagonal tile: key j*128 + col <= row
+#pragma unroll
+        for (int i = 0; i < 32; ++i) s[c * 32 + i] = (c * 32 + i <= r) ? s[c * 32 + i] : -INFINITY;
+      };
+      float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+      float corr = 1.f;
+      bool resc = false;
+#if LKV_PREFILL_SPEC
+      if (j > 0) {
+        // Speculative: exponentials against the running max while the next
+        // 32-column chunk of S streams in from TMEM (a lone warp per SMSP
+        // loads TMEM at ~24 B/clk, so a serial load of the 16 KB row slice
+        // would cost ~700 clk before the first exponential); the tile max
+        // accumulates beside them. Only a warp with a row whose tile max
+        // exceeds the running max by more than 2^8 redoes the tile.
+        tc::tmem_ld32(tl + s_col, s);
+        tc::tmem_wait_ld();
+        tc::reg_fence<32>(s);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < 3) tc::tmem_ld32(tl + s_col + (c + 1) * 32, s + (c + 1) * 32);
+          if (diag) mask(c);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], s[c * 32 + i]);
+          exps(c, m_run);
+          if (c < 3) {
+            tc::tmem_wait_ld();
+            tc::reg_fence<32>(s + (c + 1) * 32);
+          }
+        }
+        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+        const bool raise = mt > m_run + 8.f;
+        if (__any_sync(0xffffffffu, raise)) {  // warp-uniform: tcgen05.st is warp-collective
+          if (raise) {
+            corr = exp2f(m_run - mt);
+            resc = true;
+            m_run = mt;
+            l_run *= corr;
+          }
+          ls2[0] = ls2[1] = 0ull;
+          tc::tmem_wait_st();  // the speculative P stores land before they are replaced
+#pragma unroll
+          for (int c = 0; c < 4; ++c) exps(c, m_run);
+        }
+      } else
+#endif
+      {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::tmem_ld32(tl + s_col + c * 32, s + c * 32);
+        tc::tmem_wait_ld();
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tc::reg_fence<32>(s + c * 32);
+        if (diag) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) mask(c);
+        }
+#pragma unroll
+        for (int c = 0; c < 128; ++c) mx[c & 3] = fmaxf(mx[c & 3], s[c]);
+        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+        if (mt > m_run + 8.f) {  // lazy rescale
+          corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
+          resc = j > 0;
+          m_run = mt;
+          l_run *= corr;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) exps(c, m_run);  // P(j) -> TMEM over S(j), 32 columns at a time
       }
       {
         float l0, l1, l2, l3;
