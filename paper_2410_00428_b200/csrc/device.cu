@@ -647,11 +647,12 @@ struct lkv_device final : layersim::KvObserver {
   // the layer's table row (GPU slots, absolute block index) or nullptr for a
   // contiguous destination (staging).
   void scatter_blocks(const __nv_bfloat16* kb, const __nv_bfloat16* vb, long long tokens, long long b0, long long n,
-                      const int* frames, char* dst) {
+                      const int* frames, char* dst, bool reverse = false) {
     if (n <= 0) return;
     // D = 128 and bs in {16, 32, 64} (init): one CTA per K or V half slot
     scatter_slots_kernel<<<static_cast<unsigned>(2 * n), 256, 0, cs>>>(kb, vb, tokens, static_cast<int>(b0), frames,
-                                                                      dst, sb, Hl, __builtin_ctz(bs));
+                                                                      dst, sb, Hl, __builtin_ctz(bs),
+                                                                      reverse ? static_cast<int>(n) : 0);
     LKV_CUDA(cudaGetLastError());
   }
 
@@ -715,6 +716,12 @@ struct lkv_device final : layersim::KvObserver {
         throw CapacityError("CPU slot " + std::to_string(e.cpu_slot) + " >= host frames");
       tokens += e.filled_tokens;
     }
+    // Staging order = ascending CPU slot (the gather takes any GPU slot
+    // order), so runs of destination frames coalesce into single copies.
+    std::vector<long long> ord(static_cast<std::size_t>(n));
+    for (long long i = 0; i < n; ++i) ord[i] = i;
+    std::stable_sort(ord.begin(), ord.end(),
+                     [&](long long a, long long b) { return entries[a].cpu_slot < entries[b].cpu_slot; });
     // One gather launch per run of consecutive staging segments (up to the
     // ring's wrap; a CTA per slot), then one D2H per segment.
     long long i0 = 0;
@@ -725,7 +732,7 @@ struct lkv_device final : layersim::KvObserver {
       for (long long k = 0; k < nseg; ++k) next_segment();
       const long long cnt_all = std::min(nseg * seg_slots, n - i0);
       auto* slots = reinterpret_cast<unsigned*>(ring.reserve(cnt_all * sizeof(unsigned)));
-      for (long long i = 0; i < cnt_all; ++i) slots[i] = entries[i0 + i].gpu_slot;
+      for (long long i = 0; i < cnt_all; ++i) slots[i] = entries[ord[i0 + i]].gpu_slot;
       unsigned* dl = d_slotlist + seg0 * seg_slots;
       LKV_CUDA(cudaMemcpyAsync(dl, slots, cnt_all * sizeof(unsigned), cudaMemcpyHostToDevice, cs));
       ring.commit(cs);
@@ -736,7 +743,7 @@ struct lkv_device final : layersim::KvObserver {
         const long long s0 = i0 + k * seg_slots;
         const long long cnt = std::min(seg_slots, n - s0);
         std::vector<long long> cpu(cnt);
-        for (long long i = 0; i < cnt; ++i) cpu[i] = entries[s0 + i].cpu_slot;
+        for (long long i = 0; i < cnt; ++i) cpu[i] = entries[ord[s0 + i]].cpu_slot;
         d2h_segment(seg0 + static_cast<int>(k), cpu.data(), cnt);
       }
       i0 += cnt_all;
@@ -825,21 +832,26 @@ struct lkv_device final : layersim::KvObserver {
             const int seg0 = seg_next;
             for (long long k = 0; k < nseg; ++k) next_segment();
             const long long cnt_all = std::min(nseg * seg_slots, e - c0);
-            // frames == nullptr: block c0 + i -> staging slot i
-            scatter_blocks(kb, vb, tokens, c0, cnt_all, nullptr, d_staging + seg0 * seg_slots * sb);
-            for (long long k = 0; k < nseg; ++k) {
-              const long long s0 = c0 + k * seg_slots;
-              const long long cnt = std::min(seg_slots, e - s0);
-              std::vector<long long> cpu(cnt);
-              for (long long i = 0; i < cnt; ++i) {
-                const auto& en = r.blocks[s0 + i].layers[l];
-                check_slot(en);
-                cpu[i] = en.slot;
-              }
-              d2h_segment(seg0 + static_cast<int>(k), cpu.data(), cnt);
-              const long long tok_hi = std::min(tokens, (s0 + cnt) * bs);
-              ostats.d2h_bytes_algorithmic += (tok_hi - s0 * bs) * (sb / bs);
+            std::vector<long long> cpu(cnt_all);
+            for (long long i = 0; i < cnt_all; ++i) {
+              const auto& en = r.blocks[c0 + i].layers[l];
+              check_slot(en);
+              cpu[i] = en.slot;
             }
+            // block c0 + i -> staging slot i; a span whose CPU slots descend
+            // (a released request's slots popped back off the LIFO list) is
+            // packed in reverse, so staging and host frames ascend together
+            const bool rev = cnt_all > 1 && cpu.front() > cpu.back();
+            if (rev) std::reverse(cpu.begin(), cpu.end());
+            scatter_blocks(kb, vb, tokens, c0, cnt_all, nullptr, d_staging + seg0 * seg_slots * sb, rev);
+            for (long long k = 0; k < nseg; ++k) {
+              const long long p0 = k * seg_slots;
+              const long long cnt = std::min(seg_slots, cnt_all - p0);
+              if (cnt <= 0) break;
+              d2h_segment(seg0 + static_cast<int>(k), cpu.data() + p0, cnt);
+            }
+            const long long tok_hi = std::min(tokens, (c0 + cnt_all) * bs);
+            ostats.d2h_bytes_algorithmic += (tok_hi - c0 * bs) * (sb / bs);
             c0 += cnt_all;
           }
         }
@@ -1010,12 +1022,20 @@ struct lkv_device final : layersim::KvObserver {
     }
     in_iteration = true;
     if (tiered()) {
-      // read-ahead depth: as many layers as the pinned frames hold beside the
-      // ones the prefetch pipeline has in flight (and one draining)
+      // read-ahead depth: the layers staged ahead take their frames from the
+      // least recently used ones, which must already be past their DMA — a
+      // victim still in flight blocks the API thread (HostTier::take_frame
+      // waits for its event) and drains the prefetch pipeline (50% pinned,
+      // read_ahead 13: 9 GB/s). So leave the in-flight layers and as many
+      // again untouched; a few layers of lead cover the read-in latency.
       long long per_layer = 0;
       for (const Member& m : members) per_layer += m.nblk;
       const long long fit = per_layer > 0 ? cfg.pinned_frames / per_layer : L;
-      read_ahead = static_cast<int>(std::clamp<long long>(fit - cfg.pipeline_depth - 1, 0, L));
+      #ifndef LKV_TIER_RA_SLACK
+#define LKV_TIER_RA_SLACK 2
+#endif
+      read_ahead = static_cast<int>(
+          std::clamp<long long>(fit - 2 * cfg.pipeline_depth - LKV_TIER_RA_SLACK, 0, std::min(L, 6)));
       staged.assign(L, 0);
       staged_slots.assign(L, {});
       for (int l = 0; l < std::min(read_ahead + cfg.pipeline_depth, L); ++l) stage_layer(l);
@@ -1480,7 +1500,7 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));
-  lc.blockDim = dim3(320);
+  lc.blockDim = dim3(kPrefillThreads);
   lc.dynamicSmemBytes = PrefillAttn2Smem::kBytes;
   lc.stream = s;
   cudaLaunchAttribute at[1];

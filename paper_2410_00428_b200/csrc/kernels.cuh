@@ -85,7 +85,10 @@ __global__ void table_apply_kernel(const TableUpdate* __restrict__ upd, int n,
 // Scatter / pack: contiguous prefill output K,V [tokens][Hl][D] -> slots.
 // Block b (tokens [b*bs, b*bs+bs)) goes to dst + frame[b] * slot_bytes, where
 // frame = the GPU slot ids from the table mirror (retained layer, scatter)
-// or b - b0 (offloaded layer, pack into a staging segment). Tokens past
+// or b - b0 (offloaded layer, pack into a staging segment; rev_n > 0: rev_n -
+// 1 - (b - b0), the span packed in reverse so that descending CPU slots, as
+// the LIFO free list hands out a released request's slots, still meet the
+// staging in ascending order and their D2H coalesces into one copy). Tokens past
 // `tokens` in the tail block are zero-filled.
 // One CTA per half slot (K or V of block b0 + i): [Hl][bs][128] bf16, written
 // contiguously; source rows (token, head) of the prefill K/V. 32-bit index
@@ -95,11 +98,11 @@ __global__ void __launch_bounds__(256) scatter_slots_kernel(const __nv_bfloat16*
                                                             const __nv_bfloat16* __restrict__ v, long long tokens,
                                                             int b0, const int* __restrict__ frames,
                                                             char* __restrict__ dst, long long slot_bytes, int Hl,
-                                                            int bs_shift) {
+                                                            int bs_shift, int rev_n) {
   const int half = static_cast<int>(blockIdx.x & 1u);
   const int bl = static_cast<int>(blockIdx.x >> 1);
   const int b = b0 + bl;
-  const long long frame = frames ? frames[b] : bl;
+  const long long frame = frames ? frames[b] : (rev_n > 0 ? rev_n - 1 - bl : bl);
   char* out = dst + frame * slot_bytes + half * (slot_bytes >> 1);
   const __nv_bfloat16* src = half ? v : k;
   const int bs_mask = (1 << bs_shift) - 1;

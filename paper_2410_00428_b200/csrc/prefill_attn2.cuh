@@ -111,10 +111,18 @@ __device__ __forceinline__ void ex2_poly2(float xa, float xb, float& pa, float& 
 #ifndef LKV_PREFILL_SPEC
 #define LKV_PREFILL_SPEC 0
 #endif
+// LKV_PREFILL_WG3 (build-time): 384 threads in three aligned warpgroups —
+// TMA + MMA warps in warpgroup 0 at 56 registers, the two softmax warpgroups
+// at 224 (setmaxnreg) — instead of 320 threads at 168 each.
+#ifndef LKV_PREFILL_WG3
+#define LKV_PREFILL_WG3 0
+#endif
+constexpr int kPrefillThreads = LKV_PREFILL_WG3 ? 384 : 320;
+constexpr int kPrefillSoftmaxWarp0 = LKV_PREFILL_WG3 ? 4 : 2;  // first softmax warp
 #ifdef LKV_PREFILL_MAXNREG
 #define LKV_PREFILL_BOUNDS __maxnreg__(LKV_PREFILL_MAXNREG)
 #else
-#define LKV_PREFILL_BOUNDS __launch_bounds__(320, 1)
+#define LKV_PREFILL_BOUNDS __launch_bounds__(kPrefillThreads, 1)
 #endif
 template <int POLY>
 __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
@@ -177,6 +185,10 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
   tc::fence_after_sync();
   const uint32_t tmem = *tmem_slot;
 
+  if (warp < kPrefillSoftmaxWarp0) {
+#if LKV_PREFILL_WG3
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
+#endif
   if (warp == 0) {
     if (lane == 0) {
       tc::tma_prefetch_desc(&qmap);
@@ -255,9 +267,13 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
         if (j > 0) tc::mma_commit(&v_empty[(j - 1) % NS]);
       }
     }
+  }
   } else {
+#if LKV_PREFILL_WG3
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
+#endif
     // softmax: warpgroup t (0 = tile A, 1 = tile B), thread = query row
-    const int t = (warp - 2) >> 2;
+    const int t = (warp - kPrefillSoftmaxWarp0) >> 2;
     const int quad = warp & 3;
     const int r = quad * 32 + lane;
     const int qt = t == 0 ? qa : qb;

@@ -27,6 +27,7 @@
     }                                                                         \
   } while (0)
 
+
 constexpr int kIters = 4096;
 
 template <int OP>
