@@ -9,10 +9,13 @@
 // exponentials overlap the other's TMEM traffic and the MMAs of the other
 // tile, and every K/V tile loaded from HBM serves 256 query rows.
 //
-// Warps: 0 TMA (Q_A, Q_B, then the K and V rings, 2 stages each; a K stage
-// frees when both S MMAs read it, a V stage when both PVs did), 1 MMA issuer
-// + TMEM owner, 2-5 softmax of tile A, 6-9 softmax of tile B (warp w reads
-// TMEM lanes 32*(w%4)..+31).
+// Warps (three aligned warpgroups, LKV_PREFILL_WG3): 0 TMA (Q_A, Q_B, then
+// the K and V rings, 2 stages each; a K stage frees when both S MMAs read it,
+// a V stage when both PVs did), 1 MMA issuer + TMEM owner, 2-3 idle — this
+// warpgroup drops to 56 registers with setmaxnreg — then 4-7 softmax of tile
+// A and 8-11 softmax of tile B at 224 (warp w reads TMEM lanes
+// 32*(w%4)..+31). The 320-thread layout (softmax warps 2-9, 168 registers
+// each, a few spilled) is the WG3 = 0 build.
 // TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,384),
 // O_B [384,512). P (fp16 pairs, against the fp16 copy of V) overwrites the
 // first 64 columns of its S. Issue order per KV tile j:
@@ -115,7 +118,7 @@ __device__ __forceinline__ void ex2_poly2(float xa, float xb, float& pa, float& 
 // TMA + MMA warps in warpgroup 0 at 56 registers, the two softmax warpgroups
 // at 224 (setmaxnreg) — instead of 320 threads at 168 each.
 #ifndef LKV_PREFILL_WG3
-#define LKV_PREFILL_WG3 0
+#define LKV_PREFILL_WG3 1
 #endif
 constexpr int kPrefillThreads = LKV_PREFILL_WG3 ? 384 : 320;
 constexpr int kPrefillSoftmaxWarp0 = LKV_PREFILL_WG3 ? 4 : 2;  // first softmax warp
