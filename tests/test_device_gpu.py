@@ -322,3 +322,23 @@ def test_free_list_mirror_after_rng31_fuzz():
     for d in devs:
         d.close()
     assert len(checked) > 100 and checked.count(-1) == 3
+
+
+def test_offload_of_reused_slots_coalesces():
+    """A released request's CPU slots come back off the LIFO free list in
+    reverse order. The pack writes such a span into staging in reverse, so the
+    D2H is still one copy per staging segment (round 2: every other prefill in
+    the bench's a14 row issued one copy per block), and the bytes stay exact."""
+    model = sc.gqa_model(L=2, hkv=8, group=1)
+    kv, dev = sc.make(model, gpu=64, cpu=600, chunk_slots=64)
+    prompt = 16 * 60  # 60 blocks per layer, one staging segment each
+    copies = []
+    for it in range(3):
+        dev.offload_stats(reset=True)
+        sc.prefill(kv, dev, it, prompt, 0)
+        slots = [blk.layers[0].slot for blk in kv.request(it).blocks]
+        assert slots == sorted(slots) or slots == sorted(slots, reverse=True)
+        copies.append(dev.offload_stats().d2h_copies)
+        assert dev.verify_request(it, prompt, sc.SEED) == 0
+        kv.release(it)
+    assert copies == [2, 2, 2], copies  # one copy per layer, ascending or descending slots
