@@ -431,6 +431,7 @@ typedef struct lkv_host_tier_stats {
   int64_t pin_waits;        /* prefetches that waited for a read-in still running */
   int32_t read_ahead;       /* layers staged beyond the one being fetched (last decode iteration) */
   int32_t copy_threads;     /* read-in / write-back workers */
+  int64_t resident_frames;  /* frames kept resident outside the LRU order (cyclic re-fetch policy) */
 } lkv_host_tier_stats;
 LKV_API int lkv_device_host_tier_stats(const lkv_device* dev, lkv_host_tier_stats* out);
 /* Writes generator data for every entry of a request (GPU slots and host

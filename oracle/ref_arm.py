@@ -8,6 +8,10 @@ the reference arm loads no product library.
   in place into oracle/_ref/libref_layersim.so by oracle/Makefile) through its
   C shim (oracle/ref_shim.cpp), with a minimal ctypes binding of its own:
   allocate_prefill, the request's block table, plan_decode_fetch.
+* ``ref_simulated_ttft``: the reference Engine::run (engine.cpp:76-121, the
+  same compiled library) over the reference's own generate_fixed trace —
+  config 2's simulated TTFT p50/p99 as the reference computes it, timed on
+  one host core (the reference is single-threaded).
 * ``Port``: the oracle CPU port of one decode step (oracle/cpu_baseline.c):
   per (request, layer) it gathers the layer's slots from host frames into a
   contiguous arena with memcpy (the fetch the reference books,
@@ -52,6 +56,63 @@ LLAMA2_7B = (32, 32, 32, 128, 4096, 7.0e9, 2)  # reference config.cpp model_pres
 def kv_bytes_per_token_layer(model=LLAMA2_7B) -> int:
     """reference cost_model.cpp kv_bytes_per_token_layer: 2 (K, V) x Hkv x d x f."""
     return 2 * model[2] * model[3] * model[6]
+
+
+class _HardwareSpec(C.Structure):  # lkv_hardware_spec
+    _fields_ = [("flops", f64), ("hbm_bandwidth", f64), ("pcie_bandwidth", f64), ("nvlink", i32), ("n_gpus", i32),
+                ("gpu_mem", f64), ("kv_reserve_fraction", f64)]
+
+
+class _CostParams(C.Structure):  # lkv_cost_params
+    _fields_ = [("alpha", f64), ("beta", f64), ("gamma", f64), ("delta", f64)]
+
+
+class _EngineCfg(C.Structure):  # oracle/ref_shim.cpp ref_engine_cfg
+    _fields_ = [("model", _ModelSpec), ("hw", _HardwareSpec), ("cost", _CostParams), ("ttft_slo", f64),
+                ("tpot_slo", f64), ("policy_layerkv", i32), ("slo_scheduler", i32), ("gpu_blocks", i64),
+                ("cpu_blocks", i64), ("tokens_per_block", i32), ("horizon", i32), ("threshold_fraction", f64),
+                ("predictor_accuracy", f64), ("max_batch_tokens", i64), ("max_sim_time", f64),
+                ("chunk_bytes", f64), ("seed", C.c_uint64), ("force_retained_layers", i32),
+                ("invariant_checks", i32)]
+
+
+class _EngineOut(C.Structure):  # ref_engine_out
+    _fields_ = [("mean_ttft", f64), ("p50_ttft", f64), ("p99_ttft", f64), ("mean_tpot", f64), ("throughput", f64),
+                ("makespan", f64), ("d2h_jobs", i64), ("h2d_jobs", i64), ("d2h_bytes", f64), ("h2d_bytes", f64),
+                ("completed", i32), ("n_rows", i32)]
+
+
+def ref_simulated_ttft(ctx: int, n: int = 100, output: int = 512, rate: float = 1.0, seed: int = 1) -> dict:
+    """Config 2: generate_fixed(n, ctx, output, rate, seed)
+    through the reference Engine::run with the reference defaults
+    (config.cpp: L20-like HardwareSpec 1e14 / 8.64e11 / 3.2e10, 48 GB, cost
+    params 1/1/1/0.5, SLOs 3 s / 0.2 s, horizon 8) and the 48 GB-capped
+    pools 113,043 / 904,344; both policies. Host time on one core."""
+    if not os.path.exists(REF_SO):
+        raise RuntimeError(f"reference library not built: {REF_SO} (make -C oracle ref)")
+    dll = C.CDLL(REF_SO)
+    dll.ref_engine_run.restype = i32
+    dll.ref_generate_trace.restype = i32
+    dll.lkv_last_error.restype = C.c_char_p
+    ids, arr = (i64 * n)(), (f64 * n)()
+    p, o = (i32 * n)(), (i32 * n)()
+    if dll.ref_generate_trace(0, n, ctx, output, C.c_double(rate), C.c_uint64(seed), ids, arr, p, o) != 0:
+        raise RuntimeError("ref_generate_trace failed")
+    out = {"unit": "s", "source": "compiled reference Engine::run (oracle/_ref), virtual time"}
+    for pol in ("layerkv", "baseline"):
+        cfg = _EngineCfg(_ModelSpec(*LLAMA2_7B, 0), _HardwareSpec(1.0e14, 8.64e11, 3.2e10, 0, 1, 48e9, 0.9),
+                         _CostParams(1.0, 1.0, 1.0, 0.5), 3.0, 0.2, int(pol == "layerkv"), 1, 113043, 904344, 16, 8,
+                         0.05, 0.8, 131072, 86400.0, 16.0 * 1024 * 1024, seed, -1, 0)
+        res = _EngineOut()
+        ln = C.c_size_t()
+        t0 = time.perf_counter()
+        st = dll.ref_engine_run(C.byref(cfg), n, ids, arr, p, o, C.byref(res), None, C.c_size_t(0), C.byref(ln))
+        host_s = time.perf_counter() - t0
+        if st != 0:
+            raise RuntimeError("ref_engine_run: " + dll.lkv_last_error().decode())
+        out[pol] = {"p50": res.p50_ttft, "p99": res.p99_ttft, "mean_tpot": res.mean_tpot,
+                    "tokens_per_s": res.throughput, "host_s_1core": host_s}
+    return out
 
 
 class RefKvManager:

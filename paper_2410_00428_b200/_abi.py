@@ -108,7 +108,7 @@ class DeviceConfig(C.Structure):
 class HostTierStats(C.Structure):
     _fields_ = [("pinned_frames", i64), ("read_in_frames", i64), ("write_back_frames", i64), ("evictions", i64),
                 ("hits", i64), ("misses", i64), ("staged", i64), ("pin_waits", i64), ("read_ahead", i32),
-                ("copy_threads", i32)]
+                ("copy_threads", i32), ("resident_frames", i64)]
 
 
 class DeviceInfo(C.Structure):

@@ -1034,8 +1034,15 @@ struct lkv_device final : layersim::KvObserver {
       #ifndef LKV_TIER_RA_SLACK
 #define LKV_TIER_RA_SLACK 2
 #endif
+#ifndef LKV_TIER_RA_MAX
+#define LKV_TIER_RA_MAX 6
+#endif
       read_ahead = static_cast<int>(
-          std::clamp<long long>(fit - 2 * cfg.pipeline_depth - LKV_TIER_RA_SLACK, 0, std::min(L, 6)));
+          std::clamp<long long>(fit - 2 * cfg.pipeline_depth - LKV_TIER_RA_SLACK, 0, std::min(L, LKV_TIER_RA_MAX)));
+      // the rest of the frames stay resident across iterations (HostTier::
+      // set_sticky_budget): the staged layers, the one being fetched, the
+      // ones in flight and one more cycle through the LRU frames
+      tier.set_sticky_budget(cfg.pinned_frames - (read_ahead + cfg.pipeline_depth + 2) * per_layer);
       staged.assign(L, 0);
       staged_slots.assign(L, {});
       for (int l = 0; l < std::min(read_ahead + cfg.pipeline_depth, L); ++l) stage_layer(l);
@@ -1831,6 +1838,7 @@ int lkv_device_host_tier_stats(const lkv_device* d, lkv_host_tier_stats* o) {
     o->staged = t.staged;
     o->pin_waits = t.pin_waits;
     o->read_ahead = d->read_ahead;
+    o->resident_frames = d->tier.sticky_frames();
     o->copy_threads = d->tier.copy_threads();
   }
   return LKV_OK;

@@ -29,6 +29,7 @@
 #include <sys/syscall.h>
 #include <unistd.h>
 
+#include <algorithm>
 #include <atomic>
 #include <condition_variable>
 #include <cstdint>
@@ -123,6 +124,31 @@ class HostTier {
   HostTierStats stats() const {
     std::lock_guard<std::mutex> g(mu_);
     return st_;
+  }
+
+  // Up to `n` frames stay resident outside the LRU order: the next slots that
+  // take a frame keep it until the manager frees them. A decode iteration
+  // re-reads every CPU-resident slot in a fixed cyclic order, the access
+  // pattern on which LRU always evicts the slot needed next (0% hits); a
+  // fixed resident subset is the optimal policy there (hits = n / slots).
+  // The caller leaves enough LRU frames for the layers in flight and staged.
+  void set_sticky_budget(long long n) {
+    std::lock_guard<std::mutex> g(mu_);
+    sticky_budget_ = std::max(0ll, std::min(n, F_));
+    while (sticky_count_ > sticky_budget_) {  // shrink: the oldest become ordinary LRU frames
+      const int f = sticky_.front();
+      sticky_.pop_front();
+      Frame& fr = frames_[static_cast<std::size_t>(f)];
+      fr.sticky = false;
+      --sticky_count_;
+      lru_.push_front(f);
+      fr.pos = lru_.begin();
+      fr.in_lru = true;
+    }
+  }
+  long long sticky_frames() const {
+    std::lock_guard<std::mutex> g(mu_);
+    return sticky_count_;
   }
 
   // Read-ahead: make `slots` resident, starting the read-in of missing ones
@@ -255,7 +281,7 @@ class HostTier {
   };
   struct Frame {
     long long slot = -1;
-    bool dirty = false, cleaning = false, filling = false, in_lru = false;
+    bool dirty = false, cleaning = false, filling = false, in_lru = false, sticky = false;
     int locks = 0, stage_locks = 0;
     unsigned gen = 0;  // write generation
     std::shared_ptr<Ticket> last;
@@ -289,9 +315,16 @@ class HostTier {
     Frame& fr = frames_[static_cast<std::size_t>(f)];
     fr.slot = s;
     slot_frame_[static_cast<std::size_t>(s)] = f;
-    lru_.push_back(f);
-    fr.pos = std::prev(lru_.end());
-    fr.in_lru = true;
+    if (sticky_count_ < sticky_budget_) {  // kept resident: never an eviction victim
+      fr.sticky = true;
+      ++sticky_count_;
+      sticky_.push_back(f);
+      fr.pos = std::prev(sticky_.end());
+    } else {
+      lru_.push_back(f);
+      fr.pos = std::prev(lru_.end());
+      fr.in_lru = true;
+    }
     fr.filling = read && slot_valid_[static_cast<std::size_t>(s)];
     if (fr.filling) jobs.push_back(fill_job(f));
     return f;
@@ -309,6 +342,10 @@ class HostTier {
     if (fr.in_lru) {
       lru_.erase(fr.pos);
       fr.in_lru = false;
+    } else if (fr.sticky) {
+      sticky_.erase(fr.pos);
+      fr.sticky = false;
+      --sticky_count_;
     }
     free_.push_back(f);
   }
@@ -355,10 +392,11 @@ class HostTier {
           pending.clear();
         }
         bool busy = false;  // something that will make a frame evictable without this thread
-        for (int f : lru_) {
-          const Frame& fr = frames_[static_cast<std::size_t>(f)];
-          busy |= fr.cleaning || fr.filling;
-        }
+        for (const std::list<int>* l : {&lru_, &sticky_})
+          for (int f : *l) {
+            const Frame& fr = frames_[static_cast<std::size_t>(f)];
+            busy |= fr.cleaning || fr.filling;
+          }
         if (!busy)
           throw std::length_error("host tier: every pinned frame is locked by work in flight (raise pinned_frames)");
         cv_.wait(g);
@@ -499,6 +537,8 @@ class HostTier {
   std::vector<Frame> frames_;
   std::vector<int> free_;
   std::list<int> lru_;
+  std::list<int> sticky_;  // resident frames outside the LRU (set_sticky_budget)
+  long long sticky_budget_ = 0, sticky_count_ = 0;
   std::deque<int> dirty_q_;
   mutable std::mutex mu_;
   std::condition_variable cv_;

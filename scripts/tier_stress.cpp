@@ -102,8 +102,57 @@ int too_small() {
   std::_Exit(rc);  // no orderly teardown of the leaked tiers
 }
 
+// The decode iteration's access pattern (lkv_device: stage read_ahead layers
+// ahead, pin + DMA one layer, repeat every step): with a resident budget the
+// slots of the first layers must hit from the second iteration on.
+int cyclic(long long budget_layers) {
+  const int L = 16, per_layer = 64, depth = 2, ra = 2;
+  const long long slots = static_cast<long long>(L) * per_layer, frames = slots / 4;
+  lkv::HostTier tier;
+  tier.init(0, slots, frames, kSb, 4, -1);
+  auto layer_slots = [&](int l) {
+    std::vector<long long> v(per_layer);
+    for (int i = 0; i < per_layer; ++i) v[static_cast<std::size_t>(i)] = static_cast<long long>(l) * per_layer + i;
+    return v;
+  };
+  for (int l = 0; l < L; ++l) {  // every slot written once (the prefill offload)
+    auto v = layer_slots(l);
+    std::vector<long long> fr(v.size());
+    tier.pin(v.data(), per_layer, false, fr.data());
+    cudaEvent_t ev = stub_event_new();
+    stub_event_complete(ev);
+    tier.used(v.data(), per_layer, ev, true);
+  }
+  long long hits_last = 0;
+  for (int it = 0; it < 4; ++it) {
+    tier.set_sticky_budget(budget_layers * per_layer);
+    const auto h0 = tier.stats().hits;
+    std::vector<char> staged(L, 0);
+    auto stage = [&](int l) {
+      if (l >= L || staged[static_cast<std::size_t>(l)]) return;
+      staged[static_cast<std::size_t>(l)] = 1;
+      auto v = layer_slots(l);
+      tier.stage(v.data(), per_layer);
+    };
+    for (int l = 0; l < std::min(L, ra + depth); ++l) stage(l);
+    for (int l = 0; l < L; ++l) {
+      auto v = layer_slots(l);
+      std::vector<long long> fr(v.size());
+      tier.pin(v.data(), per_layer, true, fr.data());
+      cudaEvent_t ev = stub_event_new();
+      stub_event_complete(ev);
+      tier.used(v.data(), per_layer, ev, false);
+      stage(l + ra);
+    }
+    hits_last = tier.stats().hits - h0;
+    std::printf("cyclic: iteration %d, hits %lld of %lld, resident %lld\n", it, hits_last, slots, tier.sticky_frames());
+  }
+  return hits_last >= budget_layers * per_layer ? 0 : 1;
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "small") return too_small();
+  if (argc > 2 && std::string(argv[1]) == "cyclic") return cyclic(std::atoll(argv[2]));
   lkv::HostTier tier;
   tier.init(0, kSlots, kFrames, kSb, 6, -1);
   Engine eng;
@@ -123,6 +172,8 @@ int main(int argc, char** argv) {
   const int steps = 6000;
   std::vector<std::vector<long long>> staged;  // staged batches not yet pinned
   for (int step = 0; step < steps; ++step) {
+    if (step == steps / 3) tier.set_sticky_budget(kFrames / 3);  // resident subset, then shrunk
+    if (step == 2 * steps / 3) tier.set_sticky_budget(kFrames / 12);
     const int op = static_cast<int>(rng() % 10);
     if (op < 3) {  // write (prefill pack / escalation D2H / decode append)
       auto s = pick(1 + static_cast<int>(rng() % 48));
@@ -219,9 +270,9 @@ int main(int argc, char** argv) {
   }
   const auto st = tier.stats();
   std::printf("tier stress: %d ops, %lld frames checked, %lld mismatches; read-ins %lld, write-backs %lld, "
-              "evictions %lld, staged %lld, pin waits %lld\n",
+              "evictions %lld, staged %lld, pin waits %lld, hits %lld, resident %lld\n",
               steps, checked.load(), mismatches.load(), st.read_in_frames, st.write_back_frames, st.evictions,
-              st.staged, st.pin_waits);
+              st.staged, st.pin_waits, st.hits, tier.sticky_frames());
   tier.destroy();
   return mismatches.load() == 0 && checked.load() > 0 ? 0 : 1;
 }

@@ -42,3 +42,15 @@ def test_tier_concurrency_stress_cpu(tmp_path):
     r = subprocess.run([_build_tier_stress(tmp_path)], capture_output=True, text=True, timeout=300)
     assert r.returncode == 0, r.stdout + r.stderr
     assert " 0 mismatches" in r.stdout, r.stdout
+
+
+def test_tier_cyclic_refetch_keeps_resident_subset(tmp_path):
+    """The decode iteration's pattern (stage ahead, pin + DMA one layer, every
+    step): LRU gets no hits on it; a resident budget of 2 layers must give
+    2 layers of hits per iteration from the second one on."""
+    import subprocess
+    exe = _build_tier_stress(tmp_path)
+    r0 = subprocess.run([exe, "cyclic", "0"], capture_output=True, text=True, timeout=60)
+    assert r0.returncode == 0 and "iteration 3, hits 0 of" in r0.stdout, r0.stdout
+    r2 = subprocess.run([exe, "cyclic", "2"], capture_output=True, text=True, timeout=60)
+    assert r2.returncode == 0 and "iteration 3, hits 128 of 1024, resident 128" in r2.stdout, r2.stdout
