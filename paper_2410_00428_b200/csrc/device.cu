@@ -1027,7 +1027,10 @@ struct lkv_device final : layersim::KvObserver {
       // victim still in flight blocks the API thread (HostTier::take_frame
       // waits for its event) and drains the prefetch pipeline (50% pinned,
       // read_ahead 13: 9 GB/s). So leave the in-flight layers and as many
-      // again untouched; a few layers of lead cover the read-in latency.
+      // again untouched; a few layers of lead cover the read-in latency, and
+      // every frame not needed for them stays resident (below): at 50%
+      // pinned a cap of 6 layers gave 0.70-0.74 of the link, 4 or 2 gave 0.86
+      // (profiles/r2t_tier_micro.jsonl).
       long long per_layer = 0;
       for (const Member& m : members) per_layer += m.nblk;
       const long long fit = per_layer > 0 ? cfg.pinned_frames / per_layer : L;
@@ -1035,7 +1038,7 @@ struct lkv_device final : layersim::KvObserver {
 #define LKV_TIER_RA_SLACK 2
 #endif
 #ifndef LKV_TIER_RA_MAX
-#define LKV_TIER_RA_MAX 6
+#define LKV_TIER_RA_MAX 4
 #endif
       read_ahead = static_cast<int>(
           std::clamp<long long>(fit - 2 * cfg.pipeline_depth - LKV_TIER_RA_SLACK, 0, std::min(L, LKV_TIER_RA_MAX)));
