@@ -874,10 +874,22 @@ def main():
     fused = world > 1 and args.allgather == "fused"
     gathered = [torch.empty((world * B * hql * d,), dtype=torch.bfloat16, device=dev_t) for _ in range(L)] \
         if world > 1 and not fused else None
+    fused_note = None
     if fused:  # exchange gather-buffer IPC handles once; the merge kernel then stores into every rank's buffer
         handles = [None] * world
         dist.all_gather_object(handles, dev.gather_ipc_handle())
-        dev.gather_connect_ipc(handles)
+        try:
+            dev.gather_connect_ipc(handles)
+            connected = 1
+        except Exception as e:  # noqa: BLE001 — no peer path on this box: every rank falls back to NCCL
+            connected, fused_note = 0, f"fused gather not connected ({e!r}); NCCL all_gather_into_tensor used"
+        flag = torch.tensor([connected], dtype=torch.int64)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not flag.item():
+            fused = False
+            fused_note = fused_note or "fused gather not connected on every rank; NCCL all_gather_into_tensor used"
+            log(fused_note)
+            gathered = [torch.empty((world * B * hql * d,), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
         dist.barrier()
     dev.set_timing(True)
 
@@ -923,14 +935,19 @@ def main():
         place = dev.placement()
         peers = torch.tensor([place["gather_peers_p2p"]], dtype=torch.int64)
         dist.all_reduce(peers, op=dist.ReduceOp.MIN)
+        verified = bool(flag.item()) if fused else None
         multi = {"allgather": "fused peer stores in the split merge" if fused else "NCCL all_gather_into_tensor",
-                 "gather_verified": bool(flag.item()) if fused else None,
+                 "gather_verified": verified, "fallback": fused_note,
                  "gather_verified_against": ("gloo all_gather (one-GPU check)" if one_gpu else
                                              "NCCL all_gather_into_tensor of every rank's own rows") if fused else None,
                  "peers_connected": int(peers.item()), "peers_expected": 0 if one_gpu else world - 1,
                  "nccl": not one_gpu, "numa": numa, "pinned_pool_numa_node": place["numa_node"]}
-        if fused and not flag.item():
-            raise RuntimeError("fused all-gather rows differ from the reference all-gather")
+        if fused and not verified:  # loud in the line, and the timed region uses the NCCL baseline instead
+            fused = False
+            multi["allgather"] = "NCCL all_gather_into_tensor"
+            multi["fallback"] = "fused all-gather rows differed from the reference all-gather on the first step"
+            log(multi["fallback"])
+            gathered = [torch.empty((world * B * hql * d,), dtype=torch.bfloat16, device=dev_t) for _ in range(L)]
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
