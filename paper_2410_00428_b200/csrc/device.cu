@@ -1861,3 +1861,12 @@ int lkv_fill_request(lkv_device* d, int64_t id, int64_t n_tokens, uint64_t seed)
 }
 
 }  // extern "C"
+
+#if LKV_PREFILL_TRACE
+// Diagnostic builds only (scripts/build_variant.sh ... -DLKV_PREFILL_TRACE=1).
+extern "C" __attribute__((visibility("default"))) int lkv_debug_prefill_trace(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, lkv::g_pf_trace, sizeof(unsigned long long) * std::min(n, 4096)) == cudaSuccess
+             ? 0
+             : -1;
+}
+#endif

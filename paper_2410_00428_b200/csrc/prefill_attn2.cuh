@@ -106,6 +106,23 @@ __device__ __forceinline__ void ex2_poly2(float xa, float xb, float& pa, float& 
   pb = __int_as_float(__float_as_int(qb) + (__float_as_int(tb) << 23));
 }
 
+// LKV_PREFILL_TRACE (build-time, diagnostic only): clock64 stamps of CTA 0's
+// softmax and MMA phases into g_pf_trace (read by lkv_debug_prefill_trace).
+#ifndef LKV_PREFILL_TRACE
+#define LKV_PREFILL_TRACE 0
+#endif
+#if LKV_PREFILL_TRACE
+__device__ unsigned long long g_pf_trace[4096];
+#define PF_TRACE(cond, idx)                                              \
+  do {                                                                   \
+    if (blockIdx.x == 0 && (cond) && (idx) < 4096) g_pf_trace[(idx)] = clock64(); \
+  } while (0)
+#else
+#define PF_TRACE(cond, idx) \
+  do {                      \
+  } while (0)
+#endif
+
 // POLY: of every 4 column pairs, this many use ex2_poly2 (0, 1 or 2).
 // Register budget: __launch_bounds__(320, 1) lets ptxas stop at 168 (it
 // spills a few bytes there); LKV_PREFILL_MAXNREG (build-time) sets it directly.
@@ -262,9 +279,12 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
           tc::bar_wait(&k_full[j % NS], (j / NS) & 1u);
           tc::fence_after_sync();
         }
+        PF_TRACE(true, 2048 + j * 8 + 0);
         if (j > 0 && j - 1 < nt_a) pv(0, j - 1);
+        PF_TRACE(true, 2048 + j * 8 + 1);
         if (j < nt_a) qk(0, j);
         if (j > 0 && j - 1 < nt_b) pv(1, j - 1);
+        PF_TRACE(true, 2048 + j * 8 + 2);
         if (j < nt_b) qk(1, j);
         if (j < nt) tc::mma_commit(&k_empty[j % NS]);
         if (j > 0) tc::mma_commit(&v_empty[(j - 1) % NS]);
@@ -294,6 +314,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
       // completes unobserved before the barrier's next arrival).
       if (j > 0) tc::bar_wait(&o_full[t], (j - 1) & 1u);
       tc::fence_after_sync();
+      PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 0);
       const bool diag = j == qt;
       unsigned long long ls2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
       const unsigned long long sc2 = f2pack(scale_log2, scale_log2);
@@ -372,6 +393,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
         tc::tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 4; ++c) tc::reg_fence<32>(s + c * 32);
+        PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 1);
         if (diag) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) mask(c);
@@ -379,6 +401,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
 #pragma unroll
         for (int c = 0; c < 128; ++c) mx[c & 3] = fmaxf(mx[c & 3], s[c]);
         const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
+        PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 2);
         if (mt > m_run + 8.f) {  // lazy rescale
           corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
           resc = j > 0;
@@ -387,6 +410,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) exps(c, m_run);  // P(j) -> TMEM over S(j), 32 columns at a time
+        PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 3);
       }
       {
         float l0, l1, l2, l3;
@@ -411,6 +435,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
       }
       tc::tmem_wait_st();
       tc::fence_before_sync();
+      PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 4);
       tc::bar_arrive(&p_full[t]);
     }
     if (ntt > 0) {
