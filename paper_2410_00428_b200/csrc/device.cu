@@ -1869,4 +1869,9 @@ extern "C" __attribute__((visibility("default"))) int lkv_debug_prefill_trace(un
              ? 0
              : -1;
 }
+extern "C" __attribute__((visibility("default"))) int lkv_debug_prefill_cta(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, lkv::g_pf_cta, sizeof(unsigned long long) * std::min(n, 3 * 4096)) == cudaSuccess
+             ? 0
+             : -1;
+}
 #endif

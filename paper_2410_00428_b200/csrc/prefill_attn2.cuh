@@ -113,6 +113,7 @@ __device__ __forceinline__ void ex2_poly2(float xa, float xb, float& pa, float& 
 #endif
 #if LKV_PREFILL_TRACE
 __device__ unsigned long long g_pf_trace[4096];
+__device__ unsigned long long g_pf_cta[3 * 4096];  // per CTA: %globaltimer start, end, %smid
 #define PF_TRACE(cond, idx)                                              \
   do {                                                                   \
     if (blockIdx.x == 0 && (cond) && (idx) < 4096) g_pf_trace[(idx)] = clock64(); \
@@ -154,6 +155,10 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = smem_raw;
   if ((tc::saddr(sm) & 1023u) != 0u) __trap();
+#if LKV_PREFILL_TRACE
+  unsigned long long t_cta0 = 0;
+  if (threadIdx.x == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_cta0));
+#endif
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + S::kBar);
   uint64_t* q_full = bars;
   uint64_t* s_full = bars + 1;  // [2] tile A, B
@@ -473,6 +478,16 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
   tc::fence_before_sync();
   __syncthreads();
   if (warp == 1) tc::tmem_free<512>(tmem);
+#if LKV_PREFILL_TRACE
+  if (threadIdx.x == 0 && blockIdx.x < 4096) {
+    unsigned long long t1, sm_id;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+    asm volatile("{ .reg .u32 r; mov.u32 r, %%smid; cvt.u64.u32 %0, r; }" : "=l"(sm_id));
+    g_pf_cta[3 * blockIdx.x] = t_cta0;
+    g_pf_cta[3 * blockIdx.x + 1] = t1;
+    g_pf_cta[3 * blockIdx.x + 2] = sm_id;
+  }
+#endif
 }
 
 }  // namespace lkv

@@ -25,6 +25,23 @@ from paper_2410_00428_b200 import layersim as ls  # noqa: E402
 from paper_2410_00428_b200.device import DTYPE_BF16, Device, DeviceConfig  # noqa: E402
 
 
+def cta_timeline(lib, n_ctas, items_per_pair_tiles):
+    """Per-CTA %globaltimer spans (start, end, SM) of the last launch."""
+    buf = (C.c_ulonglong * (3 * 4096))()
+    assert lib.dll.lkv_debug_prefill_cta(buf, 3 * 4096) == 0
+    rows = [(buf[3 * i], buf[3 * i + 1], buf[3 * i + 2]) for i in range(min(n_ctas, 4096))]
+    t0 = min(r[0] for r in rows)
+    t1 = max(r[1] for r in rows)
+    busy = {}
+    for a, b, smid in rows:
+        busy[smid] = busy.get(smid, 0) + (b - a)
+    span = t1 - t0
+    durs = sorted(b - a for a, b, _ in rows)
+    return {"ctas": len(rows), "span_us": span / 1e3, "sm_busy_frac": sum(busy.values()) / (len(busy) * span),
+            "sms": len(busy), "cta_us_min_med_max": [durs[0] / 1e3, durs[len(durs) // 2] / 1e3, durs[-1] / 1e3],
+            "last_start_us": (max(r[0] for r in rows) - t0) / 1e3}
+
+
 def main():
     p = argparse.ArgumentParser()
     p.add_argument("--lib", required=True)
@@ -68,6 +85,8 @@ def main():
         mm["period"].append(tr[b + 8] - tr[b])
     res["mma_warp"] = {kk: statistics.median(vv) for kk, vv in mm.items()}
     res["softmax_A_vs_mma"] = "cycles (clock64, one SM)"
+    nq = (T + 127) // 128
+    res["timeline"] = cta_timeline(lib, ((nq + 1) // 2) * a.hq, None)
     print(json.dumps(res))
     dev.close()
 
