@@ -40,11 +40,6 @@ using layersim::OffloadEntry;
 using layersim::OffloadJob;
 using layersim::RequestKv;
 
-// Build-time choice of the prefill softmax's polynomial share (prefill_attn2.cuh
-// POLY; scripts/build_variant.sh builds the alternatives for A/B runs).
-#ifndef LKV_PREFILL_POLY
-#define LKV_PREFILL_POLY 0
-#endif
 
 namespace lkv {
 
@@ -1034,14 +1029,9 @@ struct lkv_device final : layersim::KvObserver {
       long long per_layer = 0;
       for (const Member& m : members) per_layer += m.nblk;
       const long long fit = per_layer > 0 ? cfg.pinned_frames / per_layer : L;
-      #ifndef LKV_TIER_RA_SLACK
-#define LKV_TIER_RA_SLACK 2
-#endif
-#ifndef LKV_TIER_RA_MAX
-#define LKV_TIER_RA_MAX 4
-#endif
+      constexpr long long kRaSlack = 2, kRaMax = 4;
       read_ahead = static_cast<int>(
-          std::clamp<long long>(fit - 2 * cfg.pipeline_depth - LKV_TIER_RA_SLACK, 0, std::min(L, LKV_TIER_RA_MAX)));
+          std::clamp<long long>(fit - 2 * cfg.pipeline_depth - kRaSlack, 0, std::min<long long>(L, kRaMax)));
       // the rest of the frames stay resident across iterations (HostTier::
       // set_sticky_budget): the staged layers, the one being fetched, the
       // ones in flight and one more cycle through the LRU frames
@@ -1506,7 +1496,7 @@ int lkv_prefill_attention(lkv_device* d, const void* q, const void* k, const voi
   const int chunk_kv = static_cast<int>(std::clamp<long long>(kL2Budget / std::max(kv_per_head, 1ll), 1, d->Hl));
   const int chunk_q = chunk_kv * d->G;
   const long long npairs_all = (nq_all + 1) / 2;
-  auto fn2 = prefill_attn2_kernel<LKV_PREFILL_POLY>;
+  auto fn2 = prefill_attn2_kernel;
   d->smem_attr(reinterpret_cast<const void*>(fn2), PrefillAttn2Smem::kBytes);
   cudaLaunchConfig_t lc{};
   lc.gridDim = dim3(static_cast<unsigned>(npairs_all * d->Hql));

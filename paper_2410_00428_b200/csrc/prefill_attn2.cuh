@@ -9,13 +9,13 @@
 // exponentials overlap the other's TMEM traffic and the MMAs of the other
 // tile, and every K/V tile loaded from HBM serves 256 query rows.
 //
-// Warps (three aligned warpgroups, LKV_PREFILL_WG3): 0 TMA (Q_A, Q_B, then
+// Warps (three aligned warpgroups): 0 TMA (Q_A, Q_B, then
 // the K and V rings, 2 stages each; a K stage frees when both S MMAs read it,
 // a V stage when both PVs did), 1 MMA issuer + TMEM owner, 2-3 idle — this
 // warpgroup drops to 56 registers with setmaxnreg — then 4-7 softmax of tile
 // A and 8-11 softmax of tile B at 224 (warp w reads TMEM lanes
-// 32*(w%4)..+31). The 320-thread layout (softmax warps 2-9, 168 registers
-// each, a few spilled) is the WG3 = 0 build.
+// 32*(w%4)..+31). (Round 1's 320-thread layout, softmax warps 2-9 at 168
+// registers with a few spilled, was 2-4% slower: DESIGN.md §4.3.1.)
 // TMEM (512 columns): S_A [0,128), S_B [128,256), O_A [256,384),
 // O_B [384,512). P (fp16 pairs, against the fp16 copy of V) overwrites the
 // first 64 columns of its S. Issue order per KV tile j:
@@ -82,30 +82,6 @@ __device__ __forceinline__ unsigned long long fadd2(unsigned long long a, unsign
   return r;
 }
 
-// 2^x for a pair on the FMA/ALU pipes (x <= ~126): round-to-nearest split
-// x = n + f with the 1.5*2^23 trick, a degree-3 fit of 2^f on [-0.5, 0.5]
-// (max relative error 1.03e-4, below fp16 P's 2^-11 rounding), n added to
-// the exponent field. x = -inf (masked) clamps to 2^-127 -> 0 in fp16.
-// ~10 issue slots per pair, none on the MUFU: takes a share of the softmax
-// exponentials off the MUFU, which bounds the softmax warpgroup.
-__device__ __forceinline__ void ex2_poly2(float xa, float xb, float& pa, float& pb) {
-  const unsigned long long magic = f2pack(12582912.f, 12582912.f), neg_magic = f2pack(-12582912.f, -12582912.f);
-  const unsigned long long m1 = f2pack(-1.f, -1.f), one = f2pack(1.f, 1.f);
-  const unsigned long long c3 = f2pack(0.05500683f, 0.05500683f), c2 = f2pack(0.2422056f, 0.2422056f),
-                           c1 = f2pack(0.69328254f, 0.69328254f);
-  const unsigned long long x = f2pack(fmaxf(xa, -127.f), fmaxf(xb, -127.f));
-  const unsigned long long t = fadd2(x, magic);      // 1.5*2^23 + n, n = rint(x)
-  const unsigned long long r = fadd2(t, neg_magic);  // n
-  const unsigned long long f = ffma2(r, m1, x);      // x - n in [-0.5, 0.5]
-  const unsigned long long p = ffma2(ffma2(ffma2(c3, f, c2), f, c1), f, one);
-  float ta, tb, qa, qb;
-  f2unpack(t, ta, tb);
-  f2unpack(p, qa, qb);
-  // (t_bits << 23) == n << 23 mod 2^32: the magic's bits shift out
-  pa = __int_as_float(__float_as_int(qa) + (__float_as_int(ta) << 23));
-  pb = __int_as_float(__float_as_int(qb) + (__float_as_int(tb) << 23));
-}
-
 // LKV_PREFILL_TRACE (build-time, diagnostic only): clock64 stamps of CTA 0's
 // softmax and MMA phases into g_pf_trace (read by lkv_debug_prefill_trace).
 #ifndef LKV_PREFILL_TRACE
@@ -124,29 +100,12 @@ __device__ unsigned long long g_pf_cta[3 * 4096];  // per CTA: %globaltimer star
   } while (0)
 #endif
 
-// POLY: of every 4 column pairs, this many use ex2_poly2 (0, 1 or 2).
-// Register budget: __launch_bounds__(320, 1) lets ptxas stop at 168 (it
-// spills a few bytes there); LKV_PREFILL_MAXNREG (build-time) sets it directly.
-// LKV_PREFILL_SPEC (build-time): exponentials of tiles after the first are
-// taken against the running max while S streams in from TMEM.
-#ifndef LKV_PREFILL_SPEC
-#define LKV_PREFILL_SPEC 0
-#endif
-// LKV_PREFILL_WG3 (build-time): 384 threads in three aligned warpgroups —
-// TMA + MMA warps in warpgroup 0 at 56 registers, the two softmax warpgroups
-// at 224 (setmaxnreg) — instead of 320 threads at 168 each.
-#ifndef LKV_PREFILL_WG3
-#define LKV_PREFILL_WG3 1
-#endif
-constexpr int kPrefillThreads = LKV_PREFILL_WG3 ? 384 : 320;
-constexpr int kPrefillSoftmaxWarp0 = LKV_PREFILL_WG3 ? 4 : 2;  // first softmax warp
-#ifdef LKV_PREFILL_MAXNREG
-#define LKV_PREFILL_BOUNDS __maxnreg__(LKV_PREFILL_MAXNREG)
-#else
-#define LKV_PREFILL_BOUNDS __launch_bounds__(kPrefillThreads, 1)
-#endif
-template <int POLY>
-__global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
+// Register split: warpgroup 0 (TMA + MMA warps) drops to 56 registers with
+// setmaxnreg, the two softmax warpgroups rise to 224 (they use 172, no
+// spills); per SMSP one warp of each: (56 + 224 + 224) x 32 <= 16 K registers.
+constexpr int kPrefillThreads = 384;
+constexpr int kPrefillSoftmaxWarp0 = 4;  // first softmax warp
+__global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
     const __grid_constant__ CUtensorMap qmap, const __grid_constant__ CUtensorMap kmap,
     const __grid_constant__ CUtensorMap vmap, void* __restrict__ out, int out_f32, int tokens, int Hq, int G,
     float scale_log2, int chunk_q) {
@@ -211,9 +170,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
   const uint32_t tmem = *tmem_slot;
 
   if (warp < kPrefillSoftmaxWarp0) {
-#if LKV_PREFILL_WG3
     asm volatile("setmaxnreg.dec.sync.aligned.u32 56;\n" ::: "memory");
-#endif
   if (warp == 0) {
     if (lane == 0) {
       tc::tma_prefetch_desc(&qmap);
@@ -297,9 +254,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
     }
   }
   } else {
-#if LKV_PREFILL_WG3
     asm volatile("setmaxnreg.inc.sync.aligned.u32 224;\n" ::: "memory");
-#endif
     // softmax: warpgroup t (0 = tile A, 1 = tile B), thread = query row
     const int t = (warp - kPrefillSoftmaxWarp0) >> 2;
     const int quad = warp & 3;
@@ -333,13 +288,7 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
         for (int i = 0; i < 16; ++i) {
           float xa, xb;
           f2unpack(ffma2(f2pack(s[c * 32 + 2 * i], s[c * 32 + 2 * i + 1]), sc2, nm2), xa, xb);
-          float a, b;
-          if ((i & 3) >= 4 - POLY) {
-            ex2_poly2(xa, xb, a, b);
-          } else {
-            a = ex2_approx(xa);
-            b = ex2_approx(xb);
-          }
+          const float a = ex2_approx(xa), b = ex2_approx(xb);
           ls2[i & 1] = fadd2(ls2[i & 1], f2pack(a, b));
           const __half2 h2 = __floats2half2_rn(a, b);
           ph[i] = *reinterpret_cast<const uint32_t*>(&h2);
@@ -353,45 +302,6 @@ __global__ void LKV_PREFILL_BOUNDS prefill_attn2_kernel(
       float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
       float corr = 1.f;
       bool resc = false;
-#if LKV_PREFILL_SPEC
-      if (j > 0) {
-        // Speculative: exponentials against the running max while the next
-        // 32-column chunk of S streams in from TMEM (a lone warp per SMSP
-        // loads TMEM at ~24 B/clk, so a serial load of the 16 KB row slice
-        // would cost ~700 clk before the first exponential); the tile max
-        // accumulates beside them. Only a warp with a row whose tile max
-        // exceeds the running max by more than 2^8 redoes the tile.
-        tc::tmem_ld32(tl + s_col, s);
-        tc::tmem_wait_ld();
-        tc::reg_fence<32>(s);
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < 3) tc::tmem_ld32(tl + s_col + (c + 1) * 32, s + (c + 1) * 32);
-          if (diag) mask(c);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) mx[i & 3] = fmaxf(mx[i & 3], s[c * 32 + i]);
-          exps(c, m_run);
-          if (c < 3) {
-            tc::tmem_wait_ld();
-            tc::reg_fence<32>(s + (c + 1) * 32);
-          }
-        }
-        const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
-        const bool raise = mt > m_run + 8.f;
-        if (__any_sync(0xffffffffu, raise)) {  // warp-uniform: tcgen05.st is warp-collective
-          if (raise) {
-            corr = exp2f(m_run - mt);
-            resc = true;
-            m_run = mt;
-            l_run *= corr;
-          }
-          ls2[0] = ls2[1] = 0ull;
-          tc::tmem_wait_st();  // the speculative P stores land before they are replaced
-#pragma unroll
-          for (int c = 0; c < 4; ++c) exps(c, m_run);
-        }
-      } else
-#endif
       {
 #pragma unroll
         for (int c = 0; c < 4; ++c) tc::tmem_ld32(tl + s_col + c * 32, s + c * 32);

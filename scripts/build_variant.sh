@@ -1,7 +1,7 @@
 #!/bin/bash
 # Build an experimental variant of liblkv.so (build-time defines only; the
 # shipped library has no runtime switches) into build/variants/<name>/.
-#   bash scripts/build_variant.sh <name> "-DLKV_PREFILL_POLY=1"
+#   bash scripts/build_variant.sh trace "-DLKV_PREFILL_TRACE=1"   (scripts/prefill_trace.py)
 set -e
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
 NAME=$1; DEFS=$2
