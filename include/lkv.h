@@ -482,6 +482,8 @@ typedef struct lkv_serve_config { /* reference EngineConfig, engine.hpp:32-50 */
   uint64_t kv_seed;          /* generator seed of the synthetic K/V */
   int32_t tp_rank;           /* KV-head shard the device executes (tp_size = hw.n_gpus) */
   int32_t pad_;
+  int64_t pinned_frames;     /* 0: every CPU slot pinned; > 0: pageable homes + this many pinned
+                                frames (the f3 tier, lkv_device_config.pinned_frames) */
 } lkv_serve_config;
 
 typedef struct lkv_serve_summary { /* MetricsReport (metrics.hpp) + transfer totals + device stats */

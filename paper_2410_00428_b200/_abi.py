@@ -82,7 +82,8 @@ class ServeConfigC(C.Structure):
                 ("predictor_accuracy", f64), ("max_batch_tokens", i64), ("max_time", f64), ("chunk_bytes", f64),
                 ("seed", u64), ("force_retained_layers", i32), ("invariant_checks", i32), ("executor", i32),
                 ("device", i32), ("dense_gemms", i32), ("prefill_attention", i32), ("verify_kv", i32),
-                ("pipeline_depth", i32), ("ffn", i64), ("host_slots", i64), ("kv_seed", u64), ("tp_rank", i32), ("pad_", i32)]
+                ("pipeline_depth", i32), ("ffn", i64), ("host_slots", i64), ("kv_seed", u64), ("tp_rank", i32), ("pad_", i32),
+                ("pinned_frames", i64)]
 
 
 class ServeSummaryC(C.Structure):

@@ -194,6 +194,10 @@ class HostTier {
       Frame& fr = frames_[static_cast<std::size_t>(f)];
       if (fr.stage_locks > 0) fr.stage_locks -= 1;
       fr.locks += 1;
+      // a writer waits for a copy home of the frame's previous version to
+      // finish (the generation count already kept such a copy from cleaning
+      // the frame; this keeps the copy from reading bytes being replaced)
+      if (!read && fr.cleaning) cv_.wait(g, [&] { return !fr.cleaning; });
       frames_out[i] = f;
     }
     g.unlock();

@@ -83,6 +83,7 @@ struct DeviceOptions {
   std::int64_t host_slots = 0;
   std::uint64_t kv_seed = 0x4C61796572ull;
   int tp_rank = 0;
+  std::int64_t pinned_frames = 0;  // > 0: tiered host memory (f3)
 };
 
 struct TraceShape {
@@ -117,6 +118,7 @@ class DeviceExecutor final : public lkv::Executor {
     dc.max_batch = max_batch_;
     dc.staging_chunks = 16;
     dc.chunk_bytes = static_cast<std::int64_t>(cfg.chunk_bytes);
+    dc.pinned_frames = o.pinned_frames > 0 ? std::min(o.pinned_frames, dc.host_slots) : 0;
     SERVE_CUDA(cudaSetDevice(o.device));
     SERVE_LKV(lkv_device_create(&ms, bs, &dc, &dev_));
     lkv::device_bind_manager(dev_, kv_);
@@ -421,6 +423,7 @@ int lkv_serve_run(const lkv_serve_config* c, int32_t n, const int64_t* ids, cons
     o.host_slots = c->host_slots;
     o.kv_seed = c->kv_seed;
     o.tp_rank = c->tp_rank;
+    o.pinned_frames = c->pinned_frames;
     if (c->tp_rank < 0 || c->tp_rank >= std::max(1, c->hw.n_gpus)) {
       lkv::set_error("invalid argument: lkv_serve_run tp_rank outside [0, hw.n_gpus)");
       return LKV_ERR_INVALID;

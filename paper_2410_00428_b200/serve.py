@@ -69,6 +69,7 @@ class ServeConfig:
     host_slots: int = 0
     kv_seed: int = 0x4C61796572
     tp_rank: int = 0  # the KV-head shard the device executes; tp_size = hw.n_gpus
+    pinned_frames: int = 0  # > 0: the f3 tier (pageable homes, this many pinned frames)
 
     def c(self) -> _abi.ServeConfigC:
         return _abi.ServeConfigC(
@@ -77,7 +78,7 @@ class ServeConfig:
             self.threshold_fraction, self.predictor_accuracy, self.max_batch_tokens, self.max_time, self.chunk_bytes,
             self.seed, self.force_retained_layers, int(self.invariant_checks), EXECUTORS[self.executor], self.device,
             int(self.dense_gemms), int(self.prefill_attention), int(self.verify_kv), self.pipeline_depth, self.ffn,
-            self.host_slots, self.kv_seed, self.tp_rank, 0)
+            self.host_slots, self.kv_seed, self.tp_rank, 0, self.pinned_frames)
 
 
 def _lib(lib=None):

@@ -90,3 +90,21 @@ def test_device_measured_escalation_completes():
     assert summary["completed"] == 1 and summary["n_rows"] == len(trace)
     assert summary["kv_words_mismatched"] == 0 and summary["requests_verified"] == len(trace)
     assert summary["escalations"] > 0
+
+
+# f1 x f3: the serving loop over the tiered host memory — every CPU slot's
+# home pageable, a bounded pool of pinned frames carrying all transfers
+# (evictions, read-ins and write-backs under the reference's schedule).
+@pytest.mark.parametrize("name,pinned", [("cfg1_x0", 1024), ("esc_small", 6000), ("te_fcfs_layerkv", 1200)])
+def test_device_virtual_tiered_host_matches_reference(engine_golden, name, pinned):
+    sc = mg.ENGINE_SCENARIOS[name]
+    cfg = serve_cfg(sc, executor="device-virtual", dense_gemms=False, prefill_attention=False, verify_kv=True)
+    cfg.pinned_frames = pinned
+    trace = product_trace(sc["trace"])
+    summary, rows, csv = serve.run(cfg, trace)
+    g = engine_golden[name]
+    assert hashlib.sha256(csv.encode()).hexdigest() == g["csv_sha256"]
+    assert {k: summary[k] for k in SUMMARY_KEYS} == g["summary"]
+    assert summary["requests_verified"] == len(trace)
+    assert summary["kv_words_mismatched"] == 0
+    assert summary["escalations"] == ESCALATIONS.get(name, 0)
