@@ -232,21 +232,23 @@ __global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
       for (int j = 0; j <= nt; ++j) {
         // PV of KV tile j-1 for each tile that covers it, each followed by
         // that tile's S of KV tile j (issue order = execution order)
+        PF_TRACE(j < 128, 2048 + j * 8 + 3);
         if (j > 0) {
           const int jp = j - 1;
           tc::bar_wait(&v_full[jp % NS], (jp / NS) & 1u);
           tc::fence_after_sync();
         }
+        PF_TRACE(j < 128, 2048 + j * 8 + 4);
         if (j < nt) {
           tc::bar_wait(&k_full[j % NS], (j / NS) & 1u);
           tc::fence_after_sync();
         }
-        PF_TRACE(true, 2048 + j * 8 + 0);
+        PF_TRACE(j < 128, 2048 + j * 8 + 0);
         if (j > 0 && j - 1 < nt_a) pv(0, j - 1);
-        PF_TRACE(true, 2048 + j * 8 + 1);
+        PF_TRACE(j < 128, 2048 + j * 8 + 1);
         if (j < nt_a) qk(0, j);
         if (j > 0 && j - 1 < nt_b) pv(1, j - 1);
-        PF_TRACE(true, 2048 + j * 8 + 2);
+        PF_TRACE(j < 128, 2048 + j * 8 + 2);
         if (j < nt_b) qk(1, j);
         if (j < nt) tc::mma_commit(&k_empty[j % NS]);
         if (j > 0) tc::mma_commit(&v_empty[(j - 1) % NS]);
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
       // completes unobserved before the barrier's next arrival).
       if (j > 0) tc::bar_wait(&o_full[t], (j - 1) & 1u);
       tc::fence_after_sync();
-      PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 0);
+      PF_TRACE(j < 128 && quad == 0 && lane == 0, t * 1024 + j * 8 + 0);
       const bool diag = j == qt;
       unsigned long long ls2[2] = {0ull, 0ull};  // (+0.f, +0.f) pairs
       const unsigned long long sc2 = f2pack(scale_log2, scale_log2);
@@ -308,7 +310,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
         tc::tmem_wait_ld();
 #pragma unroll
         for (int c = 0; c < 4; ++c) tc::reg_fence<32>(s + c * 32);
-        PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 1);
+        PF_TRACE(j < 128 && quad == 0 && lane == 0, t * 1024 + j * 8 + 1);
         if (diag) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) mask(c);
@@ -316,7 +318,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
 #pragma unroll
         for (int c = 0; c < 128; ++c) mx[c & 3] = fmaxf(mx[c & 3], s[c]);
         const float mt = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])) * scale_log2;
-        PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 2);
+        PF_TRACE(j < 128 && quad == 0 && lane == 0, t * 1024 + j * 8 + 2);
         if (mt > m_run + 8.f) {  // lazy rescale
           corr = (m_run == -INFINITY) ? 0.f : exp2f(m_run - mt);
           resc = j > 0;
@@ -325,7 +327,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) exps(c, m_run);  // P(j) -> TMEM over S(j), 32 columns at a time
-        PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 3);
+        PF_TRACE(j < 128 && quad == 0 && lane == 0, t * 1024 + j * 8 + 3);
       }
       {
         float l0, l1, l2, l3;
@@ -350,7 +352,7 @@ __global__ void __launch_bounds__(kPrefillThreads, 1) prefill_attn2_kernel(
       }
       tc::tmem_wait_st();
       tc::fence_before_sync();
-      PF_TRACE(quad == 0 && lane == 0, t * 1024 + j * 8 + 4);
+      PF_TRACE(j < 128 && quad == 0 && lane == 0, t * 1024 + j * 8 + 4);
       tc::bar_arrive(&p_full[t]);
     }
     if (ntt > 0) {

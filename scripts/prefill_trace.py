@@ -77,12 +77,16 @@ def main():
                 ph[f"{names[i]}->{names[i + 1]}"].append(tr[b + i + 1] - tr[b + i])
             ph["p_stored->next_s_ready"].append(tr[b + 8] - tr[b + 4])
         res[f"tile_{'AB'[t]}"] = {kk: statistics.median(vv) for kk, vv in ph.items() if vv}
-    mm = {"top->pvA_sA_issued": [], "pvA_sA->pvB_issued": [], "period": []}
+    mm = {"top->pvA_sA_issued": [], "pvA_sA->pvB_issued": [], "period": [], "wait_v": [], "wait_k": [],
+          "pvB_issued->next_loop": []}
     for j in range(4, min(nt - 2, 127)):
         b = 2048 + j * 8
         mm["top->pvA_sA_issued"].append(tr[b + 1] - tr[b])
         mm["pvA_sA->pvB_issued"].append(tr[b + 2] - tr[b + 1])
         mm["period"].append(tr[b + 8] - tr[b])
+        mm["wait_v"].append(tr[b + 8 + 4] - tr[b + 8 + 3])
+        mm["wait_k"].append(tr[b + 8] - tr[b + 8 + 4])
+        mm["pvB_issued->next_loop"].append(tr[b + 8 + 3] - tr[b + 2])
     res["mma_warp"] = {kk: statistics.median(vv) for kk, vv in mm.items()}
     res["softmax_A_vs_mma"] = "cycles (clock64, one SM)"
     nq = (T + 127) // 128
