@@ -1057,7 +1057,8 @@ struct lkv_device final : layersim::KvObserver {
     const int cb_min = tc_path ? tile_blocks : 1;
     // units per worker before halving the chunk: the tensor-core kernel's
     // per-unit epilogue favours fewer, longer units (measured: 4 -> 85%, 8 ->
-    // 81% on the 70B TP8 shard; flat on 8B), the CUDA-core one balances at 8
+    // 81% on the 70B TP8 shard; flat on 8B; 2 and 1 within noise of 4,
+    // profiles/r2ae_tc_units.jsonl), the CUDA-core one balances at 8
     // (profiles/r1y_decode_micro.jsonl).
     const long long per_worker = tc_path ? 4 : 8;
     while (cb > cb_min && block_heads / cb < per_worker * workers) cb >>= 1;
