@@ -168,13 +168,18 @@ def _link_copy(torch, dev, barrier=None):
             s.synchronize()
             if barrier is not None:
                 barrier()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(s)
-            for _ in range(4):
-                fn()
-            e1.record(s)
-            e1.synchronize()
-            out[name] = 4 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9
+            best = 0.0
+            for _ in range(3):  # best of 3 bursts of 4 GiB (a single burst can read a few % low)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(s)
+                for _ in range(4):
+                    fn()
+                e1.record(s)
+                e1.synchronize()
+                best = max(best, 4 * n / (e0.elapsed_time(e1) * 1e-3) / 1e9)
+                if barrier is not None:
+                    break  # concurrent: one burst, all ranks at the same moment
+            out[name] = best
     del h, d
     return out
 
