@@ -77,13 +77,16 @@ def peaks():
         return 6650.0, "fallback"
 
 
-def tensor_peak():
-    """Dense bf16 TFLOP/s: measured burst (MEASURED_PEAKS.json), else the profiling guide's fallback."""
+def tensor_peak(kind="bf16_tflops"):
+    """Dense bf16 TFLOP/s measured on this pool (MEASURED_PEAKS.json): the
+    burst figure (a kernel timed alone) or, kind="bf16_tflops_sustained", the
+    seconds-long one under the power cap; else the profiling guide's
+    fallback (1.59 burst / ~1.4 sustained PFLOP/s)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return float(json.load(f)["bf16_tflops"])
+            return float(json.load(f)[kind])
     except Exception:
-        return 2250.0
+        return 1590.0 if kind == "bf16_tflops" else 1400.0
 
 
 # ------------------------------------------------------------------ clocks
@@ -392,6 +395,23 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     dense()
     attn_ms = min(ev_ms(torch, cs, attn) for _ in range(3))
     flops = 4.0 * d * hq * T * (T + 1) / 2
+    # the same kernel back to back for ~2 s: under the 1000 W cap the clocks
+    # settle lower, so this is compared with the sustained cuBLAS figure
+    n_sus = 0
+    with ClockSampler(dev_t.index or 0) as clk_sus:
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        t_sus = time.perf_counter()
+        s0.record(cs)
+        while time.perf_counter() - t_sus < 2.0:
+            for _ in range(8):
+                attn()
+                n_sus += 1
+            torch.cuda.synchronize()
+        s1.record(cs)
+        s1.synchronize()
+    sus_ms = s0.elapsed_time(s1) / n_sus
+    sus_peak = tensor_peak("bf16_tflops_sustained")
     # whole prompt: per-layer compute, then the same with the offload of every layer
     d2h_s = dev.torch_stream("d2h")
 
@@ -445,7 +465,11 @@ def prefill_rows(torch, dev_t, link, tf_peak):
         "a20_prefill_attention": {
             "kernel": "prefill_attn2_kernel (tcgen05, causal GQA, two query tiles per CTA)", "shape": f"7B MHA 32 heads, {T} tokens, 1 layer",
             "ms": attn_ms, "tflops": flops / attn_ms / 1e9, "peak_tflops": tf_peak,
-            "frac": flops / attn_ms / 1e9 / tf_peak, "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)"},
+            "frac": flops / attn_ms / 1e9 / tf_peak, "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)",
+            "sustained": {"launches": n_sus, "ms": sus_ms, "tflops": flops / sus_ms / 1e9,
+                          "peak_tflops_sustained": sus_peak, "frac": flops / sus_ms / 1e9 / sus_peak,
+                          "clocks": clk_sus.summary(),
+                          "what": "back to back for ~2 s (power-capped); peak = MEASURED_PEAKS bf16_tflops_sustained"}},
         "a14_prefill_offload_overlap": {
             "workload": (f"1 request x {T} tokens, 7B, x=0 (all {L} layers offloaded); per layer: QKV GEMM, "
                          f"pack + D2H of the layer's K/V, tcgen05 attention, O and MLP GEMMs (cuBLAS)"),
