@@ -391,6 +391,25 @@ class HostTier {
           break;
         }
       if (victim < 0) {
+        // the resident subset yields before anything waits or fails: the
+        // budget is sized for decode iterations, and a prefill or escalation
+        // in between may need more frames than the LRU part holds
+        int keep = -1;
+        for (int f : sticky_)
+          if (evictable(frames_[static_cast<std::size_t>(f)])) {
+            keep = f;
+            break;
+          }
+        if (keep >= 0) {
+          Frame& kf = frames_[static_cast<std::size_t>(keep)];
+          sticky_.erase(kf.pos);
+          kf.sticky = false;
+          --sticky_count_;
+          lru_.push_front(keep);
+          kf.pos = lru_.begin();
+          kf.in_lru = true;
+          continue;  // it is the LRU victim now
+        }
         if (!pending.empty()) {
           submit(pending);
           pending.clear();

@@ -150,8 +150,38 @@ int cyclic(long long budget_layers) {
   return hits_last >= budget_layers * per_layer ? 0 : 1;
 }
 
+// A resident budget of nearly every frame must not starve a pin() wider
+// than the LRU part (a prefill between decode iterations): resident frames
+// yield, the pin succeeds.
+int resident_yields() {
+  lkv::HostTier tier;
+  tier.init(0, 256, 64, kSb, 2, -1);
+  tier.set_sticky_budget(60);
+  std::vector<long long> s(64), fr(64);
+  for (int i = 0; i < 64; ++i) s[static_cast<std::size_t>(i)] = i;  // fills all 64 frames, 60 resident
+  tier.pin(s.data(), 64, false, fr.data());
+  cudaEvent_t ev = stub_event_new();
+  stub_event_complete(ev);
+  tier.used(s.data(), 64, ev, true);
+  std::vector<long long> t(48), ft(48);
+  for (int i = 0; i < 48; ++i) t[static_cast<std::size_t>(i)] = 100 + i;  // 48 new slots at once
+  try {
+    tier.pin(t.data(), 48, false, ft.data());
+  } catch (const std::exception& e) {
+    std::printf("resident yields: failed: %s\n", e.what());
+    return 1;
+  }
+  cudaEvent_t ev2 = stub_event_new();
+  stub_event_complete(ev2);
+  tier.used(t.data(), 48, ev2, true);
+  std::printf("resident yields: ok, resident now %lld\n", tier.sticky_frames());
+  tier.destroy();
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc > 1 && std::string(argv[1]) == "small") return too_small();
+  if (argc > 1 && std::string(argv[1]) == "yield") return resident_yields();
   if (argc > 2 && std::string(argv[1]) == "cyclic") return cyclic(std::atoll(argv[2]));
   lkv::HostTier tier;
   tier.init(0, kSlots, kFrames, kSb, 6, -1);

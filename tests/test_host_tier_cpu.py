@@ -54,3 +54,12 @@ def test_tier_cyclic_refetch_keeps_resident_subset(tmp_path):
     assert r0.returncode == 0 and "iteration 3, hits 0 of" in r0.stdout, r0.stdout
     r2 = subprocess.run([exe, "cyclic", "2"], capture_output=True, text=True, timeout=60)
     assert r2.returncode == 0 and "iteration 3, hits 128 of 1024, resident 128" in r2.stdout, r2.stdout
+
+
+def test_tier_resident_frames_yield_to_a_wide_pin(tmp_path):
+    """A resident budget of nearly every frame (set for decode iterations)
+    must not starve a pin wider than the LRU part — a prefill in between:
+    the GPU serving soak hit 'every pinned frame is locked' here."""
+    import subprocess
+    r = subprocess.run([_build_tier_stress(tmp_path), "yield"], capture_output=True, text=True, timeout=60)
+    assert r.returncode == 0 and "resident yields: ok" in r.stdout, r.stdout + r.stderr
