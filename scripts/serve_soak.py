@@ -26,6 +26,7 @@ def main():
     p = argparse.ArgumentParser()
     p.add_argument("--n", type=int, default=24)
     p.add_argument("--seed0", type=int, default=1000)
+    p.add_argument("--models", action="store_true", help="draw 7B / 8B GQA / 70B TP8 shards and block sizes 16-64")
     a = p.parse_args()
     ref = oracle.ref_lib()
     bad = 0
@@ -38,23 +39,36 @@ def main():
         cpu_blocks = 20000
         pinned = rng.choice([0, 0, 2000, 4000])
         layerkv = rng.random() < 0.85
-        model, hw = ls.llama2_7b(), ls.default_hardware()
+        kind = rng.choice(["7b", "7b", "8b_gqa", "70b_tp8"]) if a.models else "7b"
+        bs = rng.choice([16, 16, 32, 64]) if a.models else 16
+        hw = ls.default_hardware()
+        tp_rank = 0
+        if kind == "7b":
+            model = ls.llama2_7b()
+        elif kind == "8b_gqa":
+            model = ls.llama3_8b_gqa()
+        else:  # 70B GQA sharded by KV head over 8 GPUs: this GPU runs one shard
+            model = ls.llama31_70b_gqa()
+            hw = ls.HardwareSpec(hw.flops, hw.hbm_bandwidth, hw.pcie_bandwidth, True, 8, hw.gpu_mem,
+                                 hw.kv_reserve_fraction)
+            tp_rank = rng.randrange(8)
         ids, arr, pr, out = drv.generate_trace(ref, True, n_req, 0, 0, rate, seed)
         t0 = time.perf_counter()
         try:
             ws, wcsv = drv.run_engine(ref, drv.engine_cfg_struct(model, hw, layerkv=layerkv, gpu_blocks=gpu_blocks,
-                                                                 cpu_blocks=cpu_blocks, seed=seed,
+                                                                 cpu_blocks=cpu_blocks, seed=seed, tpb=bs,
                                                                  invariant_checks=True), (ids, arr, pr, out))
         except ls.SimulationError as e:  # the reference itself rejects the case: skip it
             print(json.dumps({"seed": seed, "skipped": str(e)}), flush=True)
             continue
         cfg = serve.ServeConfig(model=model, hw=hw, layerkv=layerkv, gpu_blocks=gpu_blocks, cpu_blocks=cpu_blocks,
                                 seed=seed, invariant_checks=True, executor="device-virtual", dense_gemms=False,
-                                prefill_attention=False, verify_kv=True, pinned_frames=pinned)
+                                prefill_attention=False, verify_kv=True, pinned_frames=pinned,
+                                tokens_per_block=bs, tp_rank=tp_rank)
         s, rows, csv = serve.run(cfg, serve.Trace(ids, arr, pr, out))
         ok = csv == wcsv and s["kv_words_mismatched"] == 0 and s["requests_verified"] == len(ids)
         bad += not ok
-        print(json.dumps({"seed": seed, "requests": n_req, "rate": rate, "gpu_blocks": gpu_blocks, "pinned": pinned,
+        print(json.dumps({"seed": seed, "model": kind, "bs": bs, "tp_rank": tp_rank, "requests": n_req, "rate": rate, "gpu_blocks": gpu_blocks, "pinned": pinned,
                           "layerkv": layerkv, "escalations": s["escalations"], "decode_iterations": s["decode_iterations"],
                           "d2h_jobs": ws["d2h_jobs"], "h2d_jobs": ws["h2d_jobs"], "csv_equal": csv == wcsv,
                           "kv_words_mismatched": s["kv_words_mismatched"], "s": round(time.perf_counter() - t0, 1)}),
