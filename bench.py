@@ -640,11 +640,39 @@ def gqa_prefill_row(torch, dev_t, tf_peak, T=32768):
     attn()
     ms = min(ev_ms(torch, cs, attn) for _ in range(3))
     flops = 4.0 * 128 * 32 * T * (T + 1) / 2
+    lib = library_attention(torch, cs, q, k, v, out, flops)
     dev.close()
     return {"kernel": "prefill_attn2_kernel (tcgen05, causal GQA)",
             "shape": f"config 3, Llama-3-8B GQA Hq 32 / Hkv 8, {T} tokens, 1 layer", "ms": ms,
             "tflops": flops / ms / 1e9, "peak_tflops": tf_peak, "frac": flops / ms / 1e9 / tf_peak,
-            "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)"}
+            "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)",
+            "library_cudnn": lib, "ratio_vs_cudnn": (lib["ms"] / ms) if lib.get("ms") else None}
+
+
+def library_attention(torch, cs, q, k, v, out, flops):
+    """The same causal attention through torch SDPA restricted to cuDNN (a
+    library kernel, for comparison only: not on the product path), timed the
+    same way on the same stream, with its largest deviation from our output."""
+    try:
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        rep = q.shape[1] // k.shape[1]
+        qh = q.transpose(0, 1).unsqueeze(0).contiguous()
+        kx = k.transpose(0, 1).unsqueeze(0).repeat_interleave(rep, dim=1).contiguous()
+        vx = v.transpose(0, 1).unsqueeze(0).repeat_interleave(rep, dim=1).contiguous()
+        res = {}
+
+        def run():
+            with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+                res["o"] = torch.nn.functional.scaled_dot_product_attention(qh, kx, vx, is_causal=True,
+                                                                            scale=1.0 / math.sqrt(q.shape[2]))
+        with torch.cuda.stream(cs):
+            run()
+            ms = min(ev_ms(torch, cs, run) for _ in range(3))
+            diff = (res["o"][0].transpose(0, 1).float() - out.float()).abs().max().item()
+        return {"what": "torch SDPA, cuDNN backend only, K/V expanded to Hq heads", "ms": ms,
+                "tflops": flops / ms / 1e9, "max_abs_diff_vs_ours": diff}
+    except Exception as e:  # noqa: BLE001 - a comparison, never a reason to fail the bench
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
 
 
 def tiered_host_row(torch, dev_t, link, B=2, ctx=16384, pinned_frac=0.25, steps=3):
