@@ -143,10 +143,16 @@ struct ServeReport {
   std::int64_t d2h_jobs = 0, h2d_jobs = 0;
   double d2h_bytes = 0, h2d_bytes = 0;
   std::int64_t escalations = 0;  // plan_offload jobs submitted (engine.cpp:343-352)
+  // every bus transfer of the virtual clock in submission order (the
+  // reference's Engine::transfer_log, interconnect.hpp:26-33); empty under the
+  // measured clock
+  std::vector<layersim::TransferLogRow> transfer_log;
 
   static ServeReport summarize(std::vector<RequestRecord> rows, double makespan, bool completed, const Slo& slo);
   std::string requests_csv() const;  // metrics.cpp:91-101 format, "%.9g"
   std::string summary_json() const;  // metrics.cpp:69-88 keys
+  // transfer_log.csv of the reference CLI (tools/layersim_main.cpp:96-105)
+  std::string transfer_log_csv() const;
 };
 std::string fmt9(double v);                         // "%.9g"
 double nearest_rank(std::vector<double> v, double q);  // metrics.cpp:22-29
@@ -169,6 +175,8 @@ class Executor {
   // Transfer totals so far.
   virtual void transfer_totals(std::int64_t* d2h_jobs, double* d2h_bytes, std::int64_t* h2d_jobs,
                                double* h2d_bytes) const = 0;
+  // The virtual clock's bus transfers so far (nullptr: none kept).
+  virtual const std::vector<layersim::TransferLogRow>* transfer_log() const { return nullptr; }
   // The request's KV is about to be released (its slots return to the pools).
   virtual void before_release(std::int64_t /*id*/) {}
 
@@ -212,6 +220,7 @@ class ModelledExecutor final : public Executor {
   double decode(const std::vector<std::int64_t>& batch, std::int64_t batch_kv_tokens, double now) override;
   void transfer_totals(std::int64_t* d2h_jobs, double* d2h_bytes, std::int64_t* h2d_jobs,
                        double* h2d_bytes) const override;
+  const std::vector<layersim::TransferLogRow>* transfer_log() const override { return &log_; }
   layersim::PcieBus& bus() { return bus_; }
 
  private:
@@ -219,6 +228,7 @@ class ModelledExecutor final : public Executor {
   const ServeConfig& cfg_;
   const layersim::KvManager& kv_;
   layersim::PcieBus bus_;
+  std::vector<layersim::TransferLogRow> log_;  // bus_ appends every transfer
   std::int64_t d2h_jobs_ = 0, h2d_jobs_ = 0;
   double d2h_bytes_ = 0, h2d_bytes_ = 0;
 };

@@ -388,10 +388,8 @@ typedef struct ref_engine_out {
 
 // Trace given as arrays (id, arrival, prompt, output). requests.csv text is
 // written to csv (when cap suffices); *csv_len = its length.
-LKV_API int ref_engine_run(const ref_engine_cfg* c, int32_t n, const int64_t* ids, const double* arrival,
-                   const int32_t* prompt, const int32_t* output, ref_engine_out* out, char* csv,
-                   size_t cap, size_t* csv_len) {
-  TRY EngineConfig e;
+static EngineConfig engine_cfg(const ref_engine_cfg* c) {
+  EngineConfig e;
   e.model = M(&c->model);
   e.hw = H(&c->hw);
   e.cost = P(&c->cost);
@@ -410,10 +408,21 @@ LKV_API int ref_engine_run(const ref_engine_cfg* c, int32_t n, const int64_t* id
   e.force_retained_layers = c->force_retained_layers;
   e.invariant_checks = c->invariant_checks != 0;
   e.keep_transfer_log = true;
+  return e;
+}
+
+static Trace engine_trace(const ref_engine_cfg* c, int32_t n, const int64_t* ids, const double* arrival,
+                          const int32_t* prompt, const int32_t* output) {
   Trace t;
   t.seed = c->seed;
   for (int32_t i = 0; i < n; ++i) t.requests.push_back({ids[i], arrival[i], prompt[i], output[i]});
-  Engine eng(e, t);
+  return t;
+}
+
+LKV_API int ref_engine_run(const ref_engine_cfg* c, int32_t n, const int64_t* ids, const double* arrival,
+                   const int32_t* prompt, const int32_t* output, ref_engine_out* out, char* csv,
+                   size_t cap, size_t* csv_len) {
+  TRY Engine eng(engine_cfg(c), engine_trace(c, n, ids, arrival, prompt, output));
   MetricsReport r = eng.run();
   std::memset(out, 0, sizeof *out);
   out->mean_ttft = r.mean_ttft;
@@ -438,6 +447,29 @@ LKV_API int ref_engine_run(const ref_engine_cfg* c, int32_t n, const int64_t* id
   if (csv && cap > s.size()) {
     std::memcpy(csv, s.data(), s.size());
     csv[s.size()] = 0;
+  }
+  CATCH
+}
+
+// transfer_log.csv of the same run, as the reference CLI writes it
+// (tools/layersim_main.cpp:96-105: the CLI itself needs the absent CLI11, so
+// its few formatting lines are restated here over Engine::transfer_log()).
+LKV_API int ref_engine_transfer_log(const ref_engine_cfg* c, int32_t n, const int64_t* ids, const double* arrival,
+                            const int32_t* prompt, const int32_t* output, char* buf, size_t cap, size_t* len) {
+  TRY Engine eng(engine_cfg(c), engine_trace(c, n, ids, arrival, prompt, output));
+  eng.run();
+  std::ostringstream os;
+  os << "submit_s,start_s,end_s,bytes,direction,deferrals\n";
+  for (const auto& row : eng.transfer_log()) {
+    os << format_double(row.submit) << ',' << format_double(row.start) << ',' << format_double(row.end) << ','
+       << format_double(row.bytes) << ',' << (row.direction == Direction::DeviceToHost ? "d2h" : "h2d") << ','
+       << row.deferrals << "\n";
+  }
+  const std::string s = os.str();
+  *len = s.size();
+  if (buf && cap > s.size()) {
+    std::memcpy(buf, s.data(), s.size());
+    buf[s.size()] = 0;
   }
   CATCH
 }

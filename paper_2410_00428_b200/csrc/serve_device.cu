@@ -239,6 +239,11 @@ class DeviceExecutor final : public lkv::Executor {
   void transfer_totals(std::int64_t* a, double* b, std::int64_t* c, double* d) const override {
     modelled_.transfer_totals(a, b, c, d);
   }
+  // the virtual clock's schedule (the one the device executes); none when
+  // CUDA events are the clock
+  const std::vector<layersim::TransferLogRow>* transfer_log() const override {
+    return o_.measured ? nullptr : modelled_.transfer_log();
+  }
 
   void before_release(std::int64_t id) override {
     if (!o_.verify) return;
@@ -402,7 +407,13 @@ void from_trace(const lkv::Trace& t, int64_t* ids, double* arrival, int32_t* p, 
 int lkv_serve_run(const lkv_serve_config* c, int32_t n, const int64_t* ids, const double* arrival,
                   const int32_t* prompt, const int32_t* output, lkv_serve_summary* out, lkv_serve_request_row* rows,
                   int32_t rows_cap) {
-  if (!c || !out || n < 1 || !ids || !arrival || !prompt || !output) {
+  return lkv_serve_run_ex(c, n, ids, arrival, prompt, output, out, rows, rows_cap, nullptr, 0, nullptr);
+}
+
+int lkv_serve_run_ex(const lkv_serve_config* c, int32_t n, const int64_t* ids, const double* arrival,
+                     const int32_t* prompt, const int32_t* output, lkv_serve_summary* out, lkv_serve_request_row* rows,
+                     int32_t rows_cap, char* tlog, size_t tlog_cap, size_t* tlog_len) {
+  if (!c || !out || n < 1 || !ids || !arrival || !prompt || !output || (tlog && !tlog_len)) {
     lkv::set_error("invalid argument: lkv_serve_run");
     return LKV_ERR_INVALID;
   }
@@ -472,6 +483,14 @@ int lkv_serve_run(const lkv_serve_config* c, int32_t n, const int64_t* ids, cons
     for (std::size_t i = 0; i < r.requests.size() && static_cast<int32_t>(i) < rows_cap; ++i) {
       const auto& q = r.requests[i];
       rows[i] = {q.id, q.arrival, q.queuing, q.prefill, q.ttft, q.mean_tpot, q.output_tokens, q.violated ? 1 : 0};
+    }
+  }
+  if (tlog_len) {
+    const std::string s = r.transfer_log_csv();
+    *tlog_len = s.size();
+    if (tlog && tlog_cap > s.size()) {
+      std::memcpy(tlog, s.data(), s.size());
+      tlog[s.size()] = 0;
     }
   }
   SERVE_CATCH

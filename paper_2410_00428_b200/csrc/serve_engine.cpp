@@ -27,7 +27,9 @@ using layersim::TransferJob;
 
 // ---------------------------------------------------------------- modelled executor
 ModelledExecutor::ModelledExecutor(const ServeConfig& cfg, const KvManager& kv)
-    : cfg_(cfg), kv_(kv), bus_(cfg.cost.delta) {}
+    : cfg_(cfg), kv_(kv), bus_(cfg.cost.delta) {
+  bus_.set_log(&log_);  // the reference keeps it under keep_transfer_log (engine.cpp:59)
+}
 
 void ModelledExecutor::count(const TransferJob& job) {
   if (job.direction == Direction::DeviceToHost) {
@@ -455,6 +457,7 @@ struct ServeEngine::Impl {
     if (!completed) makespan = now;
     ServeReport rep = ServeReport::summarize(std::move(rows), makespan, completed, cfg.slo);
     exec->transfer_totals(&rep.d2h_jobs, &rep.d2h_bytes, &rep.h2d_jobs, &rep.h2d_bytes);
+    if (const auto* log = exec->transfer_log()) rep.transfer_log = *log;
     rep.escalations = escalations;
     return rep;
   }

@@ -168,6 +168,15 @@ std::string ServeReport::requests_csv() const {
   return os.str();
 }
 
+std::string ServeReport::transfer_log_csv() const {
+  std::ostringstream os;
+  os << "submit_s,start_s,end_s,bytes,direction,deferrals\n";
+  for (const layersim::TransferLogRow& t : transfer_log)
+    os << fmt9(t.submit) << ',' << fmt9(t.start) << ',' << fmt9(t.end) << ',' << fmt9(t.bytes) << ','
+       << (t.direction == layersim::Direction::DeviceToHost ? "d2h" : "h2d") << ',' << t.deferrals << '\n';
+  return os.str();
+}
+
 std::string ServeReport::summary_json() const {
   std::ostringstream os;
   os << "{\n  \"requests\": " << requests.size() << ",\n  \"completed\": " << (completed ? "true" : "false")

@@ -125,13 +125,27 @@ def requests_csv(rows, lib=None) -> str:
     return buf.raw[:ln.value].decode()
 
 
-def run(cfg: ServeConfig, trace: Trace, lib=None):
-    """Engine::run. Returns (summary dict, rows, requests.csv text)."""
+def run(cfg: ServeConfig, trace: Trace, lib=None, transfer_log=False):
+    """Engine::run. Returns (summary dict, rows, requests.csv text), and with
+    transfer_log=True also the run's transfer_log.csv text (the reference
+    CLI's --transfer-log file, tools/layersim_main.cpp:96-105)."""
     L = _lib(lib)
     n = len(trace)
     out = _abi.ServeSummaryC()
     rows = (_abi.ServeRowC * n)()
-    L.call("lkv_serve_run", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n)
+    if not transfer_log:
+        L.call("lkv_serve_run", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n)
+    else:
+        cap = 1 << 20
+        while True:  # the log's size is known only after the run: rerun once with room for it
+            buf, ln = C.create_string_buffer(cap), C.c_size_t()
+            L.call("lkv_serve_run_ex", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n, buf, cap,
+                   C.byref(ln))
+            if ln.value < cap:
+                break
+            cap = ln.value + 1
     summary = {k: getattr(out, k) for k, _ in out._fields_ if k != "pad_"}
     got = list(rows)[:out.n_rows]
+    if transfer_log:
+        return summary, got, requests_csv(got, L), buf.raw[:ln.value].decode()
     return summary, got, requests_csv(got, L)

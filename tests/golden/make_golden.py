@@ -162,7 +162,42 @@ def kv_goldens(lib):
     return res
 
 
+# transfer_log.csv goldens (f4): scenarios of ENGINE_SCENARIOS, plus PCIe-only
+# tensor parallelism (nvlink off), where all-reduce windows defer chunks and
+# the deferrals column is non-zero (interconnect.cpp check-and-delay).
+TLOG_SCENARIOS = ["cfg1_x32", "cfg1_x0", "cfg2_layerkv_1024", "cfg2_baseline_1024", "te_contended", "esc_small",
+                  "cfg4_b200_tp4", "cfg5_7b_4k_k16_bs32", "tlog_tp4_pcie", "tlog_tp2_pcie_contended"]
+TLOG_EXTRA = {
+    "tlog_tp4_pcie": {"model": "llama31_70b_gqa", "tp": 4, "nvlink": False, "pools": (2000000, 16000000),
+                      "layerkv": True, "force": 40, "trace": ("fixed", 6, 2048, 17, 4.0, 5)},
+    "tlog_tp2_pcie_contended": {"model": "llama2_7b", "tp": 2, "nvlink": False, "pools": (3000, 24000),
+                                "layerkv": True, "force": -1, "seed": 7, "trace": ("sharegpt", 40, 10.0, 17)},
+}
+
+
+def tlog_scenario(name):
+    return TLOG_EXTRA[name] if name in TLOG_EXTRA else ENGINE_SCENARIOS[name]
+
+
+def tlog_goldens(lib):
+    out = {}
+    for name in TLOG_SCENARIOS:
+        sc = tlog_scenario(name)
+        csv = drv.run_engine_transfer_log(lib, scenario_cfg(sc), make_trace(lib, sc["trace"]))
+        lines = csv.splitlines()
+        out[name] = {"sha256": hashlib.sha256(csv.encode()).hexdigest(), "rows": len(lines) - 1,
+                     "head": lines[:3], "deferred_rows": sum(1 for x in lines[1:] if not x.endswith(",0"))}
+        print(name, out[name]["rows"], out[name]["deferred_rows"], flush=True)
+    return out
+
+
 def main():
+    import sys
+    if sys.argv[1:] == ["tlog"]:
+        oracle.build()
+        with open(os.path.join(HERE, "engine_tlog.json"), "w") as f:
+            json.dump(tlog_goldens(oracle.ref_lib()), f, indent=1)
+        return
     oracle.build()
     lib = oracle.ref_lib()
     kv = kv_goldens(lib)

@@ -153,3 +153,39 @@ def test_errors_are_loud():
         serve.run(cfg, product_trace(sc["trace"]))
     with pytest.raises(ls.LkvError, match="arrivals not sorted"):
         serve.run(serve_cfg(sc), serve.Trace([0, 1], [1.0, 0.5], [4, 4], [2, 2]))
+
+
+@pytest.fixture(scope="module")
+def tlog_golden():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "engine_tlog.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", mg.TLOG_SCENARIOS)
+def test_transfer_log_matches_reference_golden(tlog_golden, name):
+    """transfer_log.csv (f4; the reference CLI's --transfer-log file over
+    Engine::transfer_log(), tools/layersim_main.cpp:96-105): every bus
+    transfer of the run — submit / start / end times, bytes, direction and
+    all-reduce deferrals — byte-identical to the compiled reference's."""
+    sc = mg.tlog_scenario(name)
+    summary, _, _, tlog = serve.run(serve_cfg(sc), product_trace(sc["trace"]), transfer_log=True)
+    g = tlog_golden[name]
+    lines = tlog.splitlines()
+    assert lines[:3] == g["head"] and len(lines) - 1 == g["rows"]
+    assert len(lines) - 1 == summary["d2h_jobs"] + summary["h2d_jobs"]
+    assert hashlib.sha256(tlog.encode()).hexdigest() == g["sha256"]
+
+
+def test_transfer_log_live_against_reference(ref):
+    """The same file from the live reference engine on a PCIe-only TP run
+    (deferred chunks), compared line by line so a mismatch names its row."""
+    if not hasattr(ref.dll, "ref_engine_transfer_log"):
+        pytest.skip("reference shim has no ref_engine_transfer_log")
+    sc = mg.tlog_scenario("tlog_tp4_pcie")
+    want = drv.run_engine_transfer_log(ref, mg.scenario_cfg(sc), mg.make_trace(ref, sc["trace"])).splitlines()
+    _, _, _, got = serve.run(serve_cfg(sc), product_trace(sc["trace"]), transfer_log=True)
+    got = got.splitlines()
+    assert len(got) == len(want)
+    for i, (a, b) in enumerate(zip(got, want)):
+        assert a == b, f"row {i}: {a} != {b}"
+    assert any(not x.endswith(",0") for x in got[1:])  # deferrals exercised
