@@ -508,16 +508,18 @@ typedef struct lkv_serve_request_row { /* one requests.csv row (metrics.hpp Requ
 LKV_API int lkv_serve_run(const lkv_serve_config* cfg, int32_t n, const int64_t* ids, const double* arrival,
                           const int32_t* prompt, const int32_t* output, lkv_serve_summary* out,
                           lkv_serve_request_row* rows, int32_t rows_cap);
-/* lkv_serve_run plus the run's transfer_log.csv (the reference CLI's
- * --transfer-log file, tools/layersim_main.cpp:96-105, over
- * Engine::transfer_log(), engine.hpp:79 / interconnect.hpp:26-33): one row per
- * bus transfer of the virtual clock, in submission order; header only under
- * LKV_SERVE_DEVICE_MEASURED. *tlog_len = bytes (no NUL), written when
- * tlog_cap > *tlog_len; tlog may be NULL to size. */
+/* lkv_serve_run plus the run's two CLI logs (tools/layersim_main.cpp:96-117):
+ * transfer_log.csv over Engine::transfer_log() (engine.hpp:79,
+ * interconnect.hpp:26-33) — one row per bus transfer of the virtual clock, in
+ * submission order, header only under LKV_SERVE_DEVICE_MEASURED — and
+ * decision_log.csv over Engine::decision_log() (engine.hpp:52-57,
+ * engine.cpp:388-390) — one row per LayerKV admission round that admitted or
+ * escalated. *len = bytes (no NUL), written when cap > *len; a buffer may be
+ * NULL to size, a len NULL to skip that log. */
 LKV_API int lkv_serve_run_ex(const lkv_serve_config* cfg, int32_t n, const int64_t* ids, const double* arrival,
                              const int32_t* prompt, const int32_t* output, lkv_serve_summary* out,
                              lkv_serve_request_row* rows, int32_t rows_cap, char* tlog, size_t tlog_cap,
-                             size_t* tlog_len);
+                             size_t* tlog_len, char* dlog, size_t dlog_cap, size_t* dlog_len);
 /* requests.csv text of rows (metrics.cpp:91-101): *len = bytes (no NUL),
  * written when cap > *len. */
 LKV_API int lkv_serve_requests_csv(const lkv_serve_request_row* rows, int32_t n, char* buf, size_t cap,

@@ -132,6 +132,15 @@ struct RequestRecord {
   bool violated = false, violated_ttft = false, violated_tpot = false;
 };
 
+// One LayerKV admission round that admitted or escalated (the reference's
+// DecisionLogRow, engine.hpp:52-57, recorded at engine.cpp:388-390).
+struct DecisionRecord {
+  double time = 0.0;
+  double min_budget = 0.0;  // smallest Eq. 2 slack; +inf when no decoding request constrains it
+  int admitted = 0;
+  Escalation plan = Escalation::None;
+};
+
 struct ServeReport {
   std::vector<RequestRecord> requests;  // ascending id
   double mean_ttft = 0, p50_ttft = 0, p99_ttft = 0, mean_tpot = 0, mean_queuing = 0, mean_prefill = 0;
@@ -147,12 +156,15 @@ struct ServeReport {
   // reference's Engine::transfer_log, interconnect.hpp:26-33); empty under the
   // measured clock
   std::vector<layersim::TransferLogRow> transfer_log;
+  std::vector<DecisionRecord> decision_log;  // LayerKV policy only
 
   static ServeReport summarize(std::vector<RequestRecord> rows, double makespan, bool completed, const Slo& slo);
   std::string requests_csv() const;  // metrics.cpp:91-101 format, "%.9g"
   std::string summary_json() const;  // metrics.cpp:69-88 keys
   // transfer_log.csv of the reference CLI (tools/layersim_main.cpp:96-105)
   std::string transfer_log_csv() const;
+  // decision_log.csv of the reference CLI (tools/layersim_main.cpp:107-117)
+  std::string decision_log_csv() const;
 };
 std::string fmt9(double v);                         // "%.9g"
 double nearest_rank(std::vector<double> v, double q);  // metrics.cpp:22-29

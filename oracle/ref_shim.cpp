@@ -408,6 +408,7 @@ static EngineConfig engine_cfg(const ref_engine_cfg* c) {
   e.force_retained_layers = c->force_retained_layers;
   e.invariant_checks = c->invariant_checks != 0;
   e.keep_transfer_log = true;
+  e.keep_decision_log = true;
   return e;
 }
 
@@ -451,19 +452,30 @@ LKV_API int ref_engine_run(const ref_engine_cfg* c, int32_t n, const int64_t* id
   CATCH
 }
 
-// transfer_log.csv of the same run, as the reference CLI writes it
-// (tools/layersim_main.cpp:96-105: the CLI itself needs the absent CLI11, so
-// its few formatting lines are restated here over Engine::transfer_log()).
-LKV_API int ref_engine_transfer_log(const ref_engine_cfg* c, int32_t n, const int64_t* ids, const double* arrival,
-                            const int32_t* prompt, const int32_t* output, char* buf, size_t cap, size_t* len) {
+// transfer_log.csv (which = 0) or decision_log.csv (which = 1) of the same
+// run, as the reference CLI writes them (tools/layersim_main.cpp:96-117: the
+// CLI itself needs the absent CLI11, so its few formatting lines are restated
+// here over Engine::transfer_log() / decision_log()).
+LKV_API int ref_engine_log(const ref_engine_cfg* c, int32_t n, const int64_t* ids, const double* arrival,
+                   const int32_t* prompt, const int32_t* output, int32_t which, char* buf, size_t cap,
+                   size_t* len) {
   TRY Engine eng(engine_cfg(c), engine_trace(c, n, ids, arrival, prompt, output));
   eng.run();
   std::ostringstream os;
-  os << "submit_s,start_s,end_s,bytes,direction,deferrals\n";
-  for (const auto& row : eng.transfer_log()) {
-    os << format_double(row.submit) << ',' << format_double(row.start) << ',' << format_double(row.end) << ','
-       << format_double(row.bytes) << ',' << (row.direction == Direction::DeviceToHost ? "d2h" : "h2d") << ','
-       << row.deferrals << "\n";
+  if (which == 0) {
+    os << "submit_s,start_s,end_s,bytes,direction,deferrals\n";
+    for (const auto& row : eng.transfer_log()) {
+      os << format_double(row.submit) << ',' << format_double(row.start) << ',' << format_double(row.end) << ','
+         << format_double(row.bytes) << ',' << (row.direction == Direction::DeviceToHost ? "d2h" : "h2d") << ','
+         << row.deferrals << "\n";
+    }
+  } else {
+    os << "time_s,min_budget_s,admitted,offload_plan\n";
+    for (const auto& row : eng.decision_log()) {
+      const char* plan = row.plan == OffloadPlanKind::None ? "none" : (row.plan == OffloadPlanKind::Half ? "half" : "full");
+      os << format_double(row.time) << ',' << format_double(row.min_budget) << ',' << row.admitted << ',' << plan
+         << "\n";
+    }
   }
   const std::string s = os.str();
   *len = s.size();

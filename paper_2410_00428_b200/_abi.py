@@ -209,7 +209,7 @@ _PROTOS = {
     # serving loop and trace formats
     "lkv_serve_run": [P(ServeConfigC), i32, P(i64), P(f64), P(i32), P(i32), P(ServeSummaryC), P(ServeRowC), i32],
     "lkv_serve_run_ex": [P(ServeConfigC), i32, P(i64), P(f64), P(i32), P(i32), P(ServeSummaryC), P(ServeRowC), i32,
-                         C.c_char_p, C.c_size_t, P(C.c_size_t)],
+                         C.c_char_p, C.c_size_t, P(C.c_size_t), C.c_char_p, C.c_size_t, P(C.c_size_t)],
     "lkv_serve_requests_csv": [P(ServeRowC), i32, C.c_char_p, C.c_size_t, P(C.c_size_t)],
     "lkv_trace_generate": [i32, i32, i32, i32, f64, u64, P(i64), P(f64), P(i32), P(i32)],
     "lkv_trace_read_jsonl": [C.c_char_p, P(i64), P(f64), P(i32), P(i32), i32, P(i32), P(i32)],

@@ -407,13 +407,15 @@ void from_trace(const lkv::Trace& t, int64_t* ids, double* arrival, int32_t* p, 
 int lkv_serve_run(const lkv_serve_config* c, int32_t n, const int64_t* ids, const double* arrival,
                   const int32_t* prompt, const int32_t* output, lkv_serve_summary* out, lkv_serve_request_row* rows,
                   int32_t rows_cap) {
-  return lkv_serve_run_ex(c, n, ids, arrival, prompt, output, out, rows, rows_cap, nullptr, 0, nullptr);
+  return lkv_serve_run_ex(c, n, ids, arrival, prompt, output, out, rows, rows_cap, nullptr, 0, nullptr, nullptr, 0,
+                          nullptr);
 }
 
 int lkv_serve_run_ex(const lkv_serve_config* c, int32_t n, const int64_t* ids, const double* arrival,
                      const int32_t* prompt, const int32_t* output, lkv_serve_summary* out, lkv_serve_request_row* rows,
-                     int32_t rows_cap, char* tlog, size_t tlog_cap, size_t* tlog_len) {
-  if (!c || !out || n < 1 || !ids || !arrival || !prompt || !output || (tlog && !tlog_len)) {
+                     int32_t rows_cap, char* tlog, size_t tlog_cap, size_t* tlog_len, char* dlog, size_t dlog_cap,
+                     size_t* dlog_len) {
+  if (!c || !out || n < 1 || !ids || !arrival || !prompt || !output || (tlog && !tlog_len) || (dlog && !dlog_len)) {
     lkv::set_error("invalid argument: lkv_serve_run");
     return LKV_ERR_INVALID;
   }
@@ -485,14 +487,16 @@ int lkv_serve_run_ex(const lkv_serve_config* c, int32_t n, const int64_t* ids, c
       rows[i] = {q.id, q.arrival, q.queuing, q.prefill, q.ttft, q.mean_tpot, q.output_tokens, q.violated ? 1 : 0};
     }
   }
-  if (tlog_len) {
-    const std::string s = r.transfer_log_csv();
-    *tlog_len = s.size();
-    if (tlog && tlog_cap > s.size()) {
-      std::memcpy(tlog, s.data(), s.size());
-      tlog[s.size()] = 0;
+  const auto put = [](const std::string& s, char* buf, size_t cap, size_t* len) {
+    if (!len) return;
+    *len = s.size();
+    if (buf && cap > s.size()) {
+      std::memcpy(buf, s.data(), s.size());
+      buf[s.size()] = 0;
     }
-  }
+  };
+  put(r.transfer_log_csv(), tlog, tlog_cap, tlog_len);
+  put(r.decision_log_csv(), dlog, dlog_cap, dlog_len);
   SERVE_CATCH
 }
 

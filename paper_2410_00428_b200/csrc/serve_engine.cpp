@@ -151,6 +151,7 @@ struct ServeEngine::Impl {
   std::vector<std::int64_t> in_batch;
   bool busy = false;
   std::int64_t escalations = 0;
+  std::vector<DecisionRecord> decisions;  // LayerKV admission rounds (decision_log.csv)
   std::int64_t threshold = 0;
   int done = 0;
 
@@ -277,6 +278,8 @@ struct ServeEngine::Impl {
       const std::int64_t n_past = r.emitted - 1;
       if (n_past >= 1) slack.push_back(prefill_slack(now - r.t_first, n_past, ranges.lo(r.range), cfg.slo));
     }
+    double min_budget = std::numeric_limits<double>::infinity();
+    for (double b : slack) min_budget = std::min(min_budget, b);
     int n;
     if (cfg.slo_scheduler) {
       std::vector<double> cost;
@@ -331,6 +334,11 @@ struct ServeEngine::Impl {
       }
     }
 
+    int admitted = 0;
+    // logged like engine.cpp:388-390, also when an admission stops the round
+    const auto log_decision = [&] {
+      if (admitted > 0 || esc != Escalation::None) decisions.push_back({now, min_budget, admitted, esc});
+    };
     for (int k = 0; k < n && n_waiting() > 0; ++k) {
       const std::int64_t i = waiting_at(0);
       const Req& r = R(i);
@@ -351,10 +359,13 @@ struct ServeEngine::Impl {
       }
       if (!ok) {
         never_fits_check(i);
+        log_decision();
         return;
       }
       admit(i, x);
+      ++admitted;
     }
+    log_decision();
   }
 
   // ---- GPU work
@@ -459,6 +470,7 @@ struct ServeEngine::Impl {
     exec->transfer_totals(&rep.d2h_jobs, &rep.d2h_bytes, &rep.h2d_jobs, &rep.h2d_bytes);
     if (const auto* log = exec->transfer_log()) rep.transfer_log = *log;
     rep.escalations = escalations;
+    rep.decision_log = decisions;
     return rep;
   }
 };

@@ -177,6 +177,15 @@ std::string ServeReport::transfer_log_csv() const {
   return os.str();
 }
 
+std::string ServeReport::decision_log_csv() const {
+  std::ostringstream os;
+  os << "time_s,min_budget_s,admitted,offload_plan\n";
+  for (const DecisionRecord& d : decision_log)
+    os << fmt9(d.time) << ',' << fmt9(d.min_budget) << ',' << d.admitted << ','
+       << (d.plan == Escalation::None ? "none" : d.plan == Escalation::Half ? "half" : "full") << '\n';
+  return os.str();
+}
+
 std::string ServeReport::summary_json() const {
   std::ostringstream os;
   os << "{\n  \"requests\": " << requests.size() << ",\n  \"completed\": " << (completed ? "true" : "false")

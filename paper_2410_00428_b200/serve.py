@@ -125,27 +125,29 @@ def requests_csv(rows, lib=None) -> str:
     return buf.raw[:ln.value].decode()
 
 
-def run(cfg: ServeConfig, trace: Trace, lib=None, transfer_log=False):
+def run(cfg: ServeConfig, trace: Trace, lib=None, logs=False):
     """Engine::run. Returns (summary dict, rows, requests.csv text), and with
-    transfer_log=True also the run's transfer_log.csv text (the reference
-    CLI's --transfer-log file, tools/layersim_main.cpp:96-105)."""
+    logs=True also the run's transfer_log.csv and decision_log.csv texts (the
+    reference CLI's --transfer-log / --decision-log files,
+    tools/layersim_main.cpp:96-117)."""
     L = _lib(lib)
     n = len(trace)
     out = _abi.ServeSummaryC()
     rows = (_abi.ServeRowC * n)()
-    if not transfer_log:
+    if not logs:
         L.call("lkv_serve_run", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n)
     else:
-        cap = 1 << 20
-        while True:  # the log's size is known only after the run: rerun once with room for it
+        cap, dcap = 1 << 20, 1 << 16
+        while True:  # the logs' sizes are known only after the run: rerun once with room for them
             buf, ln = C.create_string_buffer(cap), C.c_size_t()
+            dbuf, dln = C.create_string_buffer(dcap), C.c_size_t()
             L.call("lkv_serve_run_ex", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n, buf, cap,
-                   C.byref(ln))
-            if ln.value < cap:
+                   C.byref(ln), dbuf, dcap, C.byref(dln))
+            if ln.value < cap and dln.value < dcap:
                 break
-            cap = ln.value + 1
+            cap, dcap = max(cap, ln.value + 1), max(dcap, dln.value + 1)
     summary = {k: getattr(out, k) for k, _ in out._fields_ if k != "pad_"}
     got = list(rows)[:out.n_rows]
-    if transfer_log:
-        return summary, got, requests_csv(got, L), buf.raw[:ln.value].decode()
+    if logs:
+        return summary, got, requests_csv(got, L), buf.raw[:ln.value].decode(), dbuf.raw[:dln.value].decode()
     return summary, got, requests_csv(got, L)

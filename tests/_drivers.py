@@ -191,19 +191,21 @@ def run_engine(lib, cfg, trace):
     return summary, buf.raw[:ln.value].decode()
 
 
-def run_engine_transfer_log(lib, cfg, trace):
-    """The reference run's transfer_log.csv (Engine::transfer_log() in the CLI's
-    format, tools/layersim_main.cpp:96-105) through the shim."""
+def run_engine_log(lib, cfg, trace, which):
+    """The reference run's transfer_log.csv (which="transfer") or
+    decision_log.csv (which="decision"), Engine::transfer_log() /
+    decision_log() in the CLI's format (tools/layersim_main.cpp:96-117),
+    through the shim."""
     import ctypes as C
     ids, arr, p, o = trace
     n = len(ids)
     ln = C.c_size_t()
     args = [C.byref(cfg), n, (C.c_int64 * n)(*ids), (C.c_double * n)(*arr), (C.c_int32 * n)(*p),
-            (C.c_int32 * n)(*o)]
-    if lib.dll.ref_engine_transfer_log(*args, None, 0, C.byref(ln)) != 0:
+            (C.c_int32 * n)(*o), 0 if which == "transfer" else 1]
+    if lib.dll.ref_engine_log(*args, None, 0, C.byref(ln)) != 0:
         raise ls.SimulationError(lib.dll.lkv_last_error().decode())
     buf = C.create_string_buffer(ln.value + 1)
-    lib.dll.ref_engine_transfer_log(*args, buf, ln.value + 1, C.byref(ln))
+    lib.dll.ref_engine_log(*args, buf, ln.value + 1, C.byref(ln))
     return buf.raw[:ln.value].decode()
 
 

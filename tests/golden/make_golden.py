@@ -162,7 +162,7 @@ def kv_goldens(lib):
     return res
 
 
-# transfer_log.csv goldens (f4): scenarios of ENGINE_SCENARIOS, plus PCIe-only
+# transfer_log.csv / decision_log.csv goldens (f4, SURVEY §5 tracing): scenarios of ENGINE_SCENARIOS, plus PCIe-only
 # tensor parallelism (nvlink off), where all-reduce windows defer chunks and
 # the deferrals column is non-zero (interconnect.cpp check-and-delay).
 TLOG_SCENARIOS = ["cfg1_x32", "cfg1_x0", "cfg2_layerkv_1024", "cfg2_baseline_1024", "te_contended", "esc_small",
@@ -180,22 +180,27 @@ def tlog_scenario(name):
 
 
 def tlog_goldens(lib):
-    out = {}
+    out = {"transfer": {}, "decision": {}}
     for name in TLOG_SCENARIOS:
         sc = tlog_scenario(name)
-        csv = drv.run_engine_transfer_log(lib, scenario_cfg(sc), make_trace(lib, sc["trace"]))
-        lines = csv.splitlines()
-        out[name] = {"sha256": hashlib.sha256(csv.encode()).hexdigest(), "rows": len(lines) - 1,
-                     "head": lines[:3], "deferred_rows": sum(1 for x in lines[1:] if not x.endswith(",0"))}
-        print(name, out[name]["rows"], out[name]["deferred_rows"], flush=True)
+        for which in ("transfer", "decision"):
+            csv = drv.run_engine_log(lib, scenario_cfg(sc), make_trace(lib, sc["trace"]), which)
+            lines = csv.splitlines()
+            g = {"sha256": hashlib.sha256(csv.encode()).hexdigest(), "rows": len(lines) - 1, "head": lines[:3]}
+            if which == "transfer":
+                g["deferred_rows"] = sum(1 for x in lines[1:] if not x.endswith(",0"))
+            else:
+                g["escalating_rows"] = sum(1 for x in lines[1:] if not x.endswith(",none"))
+            out[which][name] = g
+        print(name, out["transfer"][name]["rows"], out["decision"][name]["rows"], flush=True)
     return out
 
 
 def main():
     import sys
-    if sys.argv[1:] == ["tlog"]:
+    if sys.argv[1:] == ["logs"]:
         oracle.build()
-        with open(os.path.join(HERE, "engine_tlog.json"), "w") as f:
+        with open(os.path.join(HERE, "engine_logs.json"), "w") as f:
             json.dump(tlog_goldens(oracle.ref_lib()), f, indent=1)
         return
     oracle.build()

@@ -63,18 +63,19 @@ def test_device_virtual_matches_reference_and_bytes(engine_golden, name, tp_rank
 
 
 @pytest.mark.parametrize("name", ["esc_small", "cfg4_b200_tp4", "tlog_tp4_pcie"])
-def test_device_virtual_transfer_log_matches_reference(name):
+def test_device_virtual_cli_logs_match_reference(name):
     """f4 on the device executor: the GPU moves the bytes, and the run's
     transfer_log.csv (the virtual clock's bus schedule the device executes)
-    is still the reference's byte for byte, including all-reduce deferrals on
-    PCIe-only TP."""
-    with open(os.path.join(os.path.dirname(__file__), "golden", "engine_tlog.json")) as f:
-        g = json.load(f)[name]
+    and decision_log.csv are still the reference's byte for byte, including
+    all-reduce deferrals on PCIe-only TP and escalations."""
+    with open(os.path.join(os.path.dirname(__file__), "golden", "engine_logs.json")) as f:
+        g = json.load(f)
     sc = mg.tlog_scenario(name)
     cfg = serve_cfg(sc, executor="device-virtual", dense_gemms=False, prefill_attention=False, verify_kv=True)
     trace = product_trace(sc["trace"])
-    summary, _, _, tlog = serve.run(cfg, trace, transfer_log=True)
-    assert hashlib.sha256(tlog.encode()).hexdigest() == g["sha256"]
+    summary, _, _, tlog, dlog = serve.run(cfg, trace, logs=True)
+    assert hashlib.sha256(tlog.encode()).hexdigest() == g["transfer"][name]["sha256"]
+    assert hashlib.sha256(dlog.encode()).hexdigest() == g["decision"][name]["sha256"]
     assert summary["kv_words_mismatched"] == 0 and summary["requests_verified"] == len(trace)
 
 

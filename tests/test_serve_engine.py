@@ -156,36 +156,46 @@ def test_errors_are_loud():
 
 
 @pytest.fixture(scope="module")
-def tlog_golden():
-    with open(os.path.join(os.path.dirname(__file__), "golden", "engine_tlog.json")) as f:
+def logs_golden():
+    with open(os.path.join(os.path.dirname(__file__), "golden", "engine_logs.json")) as f:
         return json.load(f)
 
 
 @pytest.mark.parametrize("name", mg.TLOG_SCENARIOS)
-def test_transfer_log_matches_reference_golden(tlog_golden, name):
-    """transfer_log.csv (f4; the reference CLI's --transfer-log file over
-    Engine::transfer_log(), tools/layersim_main.cpp:96-105): every bus
-    transfer of the run — submit / start / end times, bytes, direction and
-    all-reduce deferrals — byte-identical to the compiled reference's."""
+def test_cli_logs_match_reference_golden(logs_golden, name):
+    """The reference CLI's two logs (f4; SURVEY §5 tracing), byte-identical to
+    the compiled reference's: transfer_log.csv (every bus transfer — submit /
+    start / end, bytes, direction, all-reduce deferrals; Engine::transfer_log(),
+    tools/layersim_main.cpp:96-105) and decision_log.csv (every LayerKV
+    admission round that admitted or escalated — time, smallest Eq. 2 slack,
+    admitted count, Half/Full plan; engine.cpp:388-390, layersim_main.cpp:107-117)."""
     sc = mg.tlog_scenario(name)
-    summary, _, _, tlog = serve.run(serve_cfg(sc), product_trace(sc["trace"]), transfer_log=True)
-    g = tlog_golden[name]
-    lines = tlog.splitlines()
-    assert lines[:3] == g["head"] and len(lines) - 1 == g["rows"]
-    assert len(lines) - 1 == summary["d2h_jobs"] + summary["h2d_jobs"]
-    assert hashlib.sha256(tlog.encode()).hexdigest() == g["sha256"]
+    summary, _, _, tlog, dlog = serve.run(serve_cfg(sc), product_trace(sc["trace"]), logs=True)
+    for which, text in (("transfer", tlog), ("decision", dlog)):
+        g = logs_golden[which][name]
+        lines = text.splitlines()
+        assert lines[:3] == g["head"] and len(lines) - 1 == g["rows"], which
+        assert hashlib.sha256(text.encode()).hexdigest() == g["sha256"], which
+    assert len(tlog.splitlines()) - 1 == summary["d2h_jobs"] + summary["h2d_jobs"]
+    assert sum(1 for x in dlog.splitlines()[1:] if not x.endswith(",none")) == \
+        logs_golden["decision"][name]["escalating_rows"]
 
 
-def test_transfer_log_live_against_reference(ref):
-    """The same file from the live reference engine on a PCIe-only TP run
-    (deferred chunks), compared line by line so a mismatch names its row."""
-    if not hasattr(ref.dll, "ref_engine_transfer_log"):
-        pytest.skip("reference shim has no ref_engine_transfer_log")
-    sc = mg.tlog_scenario("tlog_tp4_pcie")
-    want = drv.run_engine_transfer_log(ref, mg.scenario_cfg(sc), mg.make_trace(ref, sc["trace"])).splitlines()
-    _, _, _, got = serve.run(serve_cfg(sc), product_trace(sc["trace"]), transfer_log=True)
-    got = got.splitlines()
+@pytest.mark.parametrize("name,which", [("tlog_tp4_pcie", "transfer"), ("esc_small", "decision"),
+                                        ("tlog_tp2_pcie_contended", "decision")])
+def test_cli_logs_live_against_reference(ref, name, which):
+    """The same files from the live reference engine, compared line by line so
+    a mismatch names its row (PCIe-only TP: deferred chunks; escalations)."""
+    if not hasattr(ref.dll, "ref_engine_log"):
+        pytest.skip("reference shim has no ref_engine_log")
+    sc = mg.tlog_scenario(name)
+    want = drv.run_engine_log(ref, mg.scenario_cfg(sc), mg.make_trace(ref, sc["trace"]), which).splitlines()
+    _, _, _, tlog, dlog = serve.run(serve_cfg(sc), product_trace(sc["trace"]), logs=True)
+    got = (tlog if which == "transfer" else dlog).splitlines()
     assert len(got) == len(want)
     for i, (a, b) in enumerate(zip(got, want)):
-        assert a == b, f"row {i}: {a} != {b}"
-    assert any(not x.endswith(",0") for x in got[1:])  # deferrals exercised
+        assert a == b, f"{which} row {i}: {a} != {b}"
+    if which == "transfer":
+        assert any(not x.endswith(",0") for x in got[1:])  # deferrals exercised
+    else:
+        assert any(not x.endswith(",none") for x in got[1:])  # escalations exercised
