@@ -199,3 +199,21 @@ def test_cli_logs_live_against_reference(ref, name, which):
         assert any(not x.endswith(",0") for x in got[1:])  # deferrals exercised
     else:
         assert any(not x.endswith(",none") for x in got[1:])  # escalations exercised
+
+
+@pytest.mark.parametrize("max_time", [5.0, 20.0])
+def test_wall_clock_cap_matches_reference(ref, max_time):
+    """max_sim_time (engine.cpp:82-86, SURVEY §5 failure detection): a run cut
+    at the cap reports completed = 0 and the same truncated requests.csv,
+    summary and both CLI logs as the reference."""
+    sc = dict(mg.ENGINE_SCENARIOS["te_contended"])
+    trace = mg.make_trace(ref, sc["trace"])
+    rcfg = mg.scenario_cfg(sc)
+    rcfg.max_sim_time = max_time
+    want_summary, want_csv = drv.run_engine(ref, rcfg, trace)
+    want_t = drv.run_engine_log(ref, rcfg, trace, "transfer")
+    want_d = drv.run_engine_log(ref, rcfg, trace, "decision")
+    summary, _, csv, tlog, dlog = serve.run(serve_cfg(sc, max_time=max_time), product_trace(sc["trace"]), logs=True)
+    assert want_summary["completed"] == 0 and summary["completed"] == 0
+    assert {k: summary[k] for k in SUMMARY_KEYS} == want_summary
+    assert csv == want_csv and tlog == want_t and dlog == want_d
