@@ -217,3 +217,22 @@ def test_wall_clock_cap_matches_reference(ref, max_time):
     assert want_summary["completed"] == 0 and summary["completed"] == 0
     assert {k: summary[k] for k in SUMMARY_KEYS} == want_summary
     assert csv == want_csv and tlog == want_t and dlog == want_d
+
+
+def test_block_starvation_matches_reference(ref):
+    """The starvation detector (engine.cpp:107-119): SURVEY §4's
+    acceptance c8 run 53 — baseline policy, 16 layers, 302 GPU blocks; the
+    request's 80 prompt blocks pass the never-fits check, but with its growth
+    reserve (19 rows x 16 layers) it never admits, so the loop runs dry. The
+    product raises the reference's exact message."""
+    m = ls.ModelSpec(16, 4, 4, 32, 128, 1e8, 2)
+    hw = ls.default_hardware()
+    trace = ([0], [0.0], [78], [287])
+    rcfg = drv.engine_cfg_struct(m, hw, layerkv=False, gpu_blocks=302, cpu_blocks=2416)
+    with pytest.raises(ls.SimulationError) as want:
+        drv.run_engine(ref, rcfg, trace)
+    cfg = serve.ServeConfig(model=m, hw=hw, layerkv=False, gpu_blocks=302, cpu_blocks=2416)
+    with pytest.raises(ls.SimulationError) as got:
+        serve.run(cfg, serve.Trace(*[list(x) for x in trace]))
+    assert "block starvation" in str(want.value)
+    assert str(got.value) == "lkv_serve_run: " + str(want.value)  # the C ABI names its entry point
