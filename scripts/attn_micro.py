@@ -32,16 +32,20 @@ def main():
     p.add_argument("--offloaded", action="store_true", help="every layer CPU-resident: per-layer H2D prefetch "
                    "runs beside the kernels, as in the bench step")
     p.add_argument("--idle-ms", type=float, default=0.0, help="leave the GPU idle this long before each layer")
+    p.add_argument("--lib", default=None, help="an alternative liblkv.so (scripts/build_variant.sh)")
+    p.add_argument("--label", default="default")
     a = p.parse_args()
+    from paper_2410_00428_b200 import _abi
+    lib = _abi.Lib(a.lib) if a.lib else None
     hkv = a.hkv or (32 if a.group == 1 else 8)
     model = ls.ModelSpec(a.layers, hkv * a.group, hkv, 128, hkv * a.group * 128, 7e9, 2)
     nblk = (a.ctx + a.bs - 1) // a.bs
     slots = a.batch * nblk * a.layers
     gslots, hslots = (64, slots + 64) if a.offloaded else (slots + 64, 64)
-    kv = ls.KvManager(ls.BlockPools(gslots, hslots, a.bs), model)
+    kv = ls.KvManager(ls.BlockPools(gslots, hslots, a.bs), model, lib=lib)
     cfg = DeviceConfig(gpu_slots=gslots, host_slots=hslots, arena_slots=a.batch * nblk + 8, max_requests=a.batch + 1,
                        max_blocks=nblk + 4, max_batch=a.batch, pipeline_depth=2)
-    dev = Device(kv, model, a.bs, cfg)
+    dev = Device(kv, model, a.bs, cfg, lib=lib)
     ids = list(range(a.batch))
     for r in ids:
         assert kv.allocate_prefill(r, a.ctx, 0 if a.offloaded else a.layers)
@@ -66,7 +70,7 @@ def main():
             kres.append(st.attn_ms / st.attn_launches)
     kvb = a.batch * a.ctx * 2 * hkv * 128 * 2
     ms = min(res)
-    print(json.dumps({"variant": "default",
+    print(json.dumps({"variant": a.label,
                       "offloaded": a.offloaded, "idle_ms": a.idle_ms, "merge_ms": ms - min(kres),
                       "group": a.group, "hkv": hkv, "batch": a.batch, "ctx": a.ctx, "bs": a.bs,
                       "ms_per_layer": ms, "kernel_ms": min(kres), "kernel_ms_mean": sum(kres) / len(kres), "kernel_span_ms": min(kspan), "GBps": kvb / (ms / 1e3) / 1e9,
