@@ -170,6 +170,22 @@ def test_attention_parity_bench_shape_g1(mode):
     dev.close()
 
 
+@pytest.mark.parametrize("mode", [None, "rising"])
+def test_attention_parity_70b_tp8_shard(mode):
+    """Config 4's per-GPU shard at the a18 bench row's context: Llama-3.1-70B
+    heads at TP 8, rank 7 (one KV head and its 8 query heads: G = 8 on the
+    tcgen05 decode tile), 12 x 32768 tokens, layers GPU-resident, every query
+    head of the last layer against the oracle (peaked softmax with "rising")."""
+    model = ls.ModelSpec(2, 64, 8, 128, 8192, 70.6e9, 2)
+    B, T, nblk = 12, 32768, 2048
+    kv, dev = sc.make(model, gpu=B * nblk * 2 + 64, cpu=64, tp_rank=7, tp_size=8, max_blocks=nblk + 8,
+                      max_batch=B, arena=B * nblk + 16)
+    for rid in range(B):
+        sc.prefill(kv, dev, rid, T, 2)
+    sc.check_attention(dev, list(range(B)), [T] * B, layers=[1], q_mode=mode)
+    dev.close()
+
+
 def test_attention_bf16_output():
     model = sc.gqa_model(L=2, hkv=8, group=4)
     kv, dev = sc.make(model)
