@@ -236,3 +236,28 @@ def test_block_starvation_matches_reference(ref):
         serve.run(cfg, serve.Trace(*[list(x) for x in trace]))
     assert "block starvation" in str(want.value)
     assert str(got.value) == "lkv_serve_run: " + str(want.value)  # the C ABI names its entry point
+
+
+def test_serve_run_ex_sizes_and_rejects_bad_log_arguments():
+    """lkv_serve_run_ex: NULL buffers size the logs (header-only logs for a
+    run without transfers), a buffer without its length pointer is rejected,
+    and a NULL length skips that log."""
+    import ctypes as C
+    from paper_2410_00428_b200 import _abi
+    L = serve._lib(None)
+    sc = mg.ENGINE_SCENARIOS["cfg1_x32"]  # everything retained: no transfers, one admission
+    cfg, trace = serve_cfg(sc), product_trace(sc["trace"])
+    n = len(trace)
+    out, rows = _abi.ServeSummaryC(), (_abi.ServeRowC * n)()
+    tl, dl = C.c_size_t(), C.c_size_t()
+    L.call("lkv_serve_run_ex", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n, None, 0, C.byref(tl),
+           None, 0, C.byref(dl))
+    assert tl.value == len("submit_s,start_s,end_s,bytes,direction,deferrals\n")
+    assert dl.value == len("time_s,min_budget_s,admitted,offload_plan\n") + len("0,inf,1,none\n")
+    buf = C.create_string_buffer(64)
+    with pytest.raises(ls.LkvError, match="invalid argument"):
+        L.call("lkv_serve_run_ex", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n, buf, 64, None,
+               None, 0, None)
+    L.call("lkv_serve_run_ex", C.byref(cfg.c()), n, *trace.arrays(), C.byref(out), rows, n, None, 0, None, None, 0,
+           None)
+    assert out.completed == 1
