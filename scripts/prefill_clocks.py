@@ -27,6 +27,7 @@ def main():
     p.add_argument("--label", default="product")
     p.add_argument("--tokens", type=int, default=32768)
     p.add_argument("--seconds", type=float, default=4.0)
+    p.add_argument("--cudnn", action="store_true", help="time torch SDPA (cuDNN backend, K/V expanded) instead")
     a = p.parse_args()
     lib = _abi.Lib(a.lib) if a.lib else None
     model = ls.ModelSpec(1, 32, 8, 128, 4096, 8e9, 2)
@@ -39,6 +40,15 @@ def main():
     v = (torch.rand((T, 8, 128), device="cuda") * 2 - 1).to(torch.bfloat16)
     out = torch.empty_like(q)
     run = lambda: dev.prefill_attention(q, k, v, out, T, 1 / math.sqrt(128), DTYPE_BF16)  # noqa: E731
+    if a.cudnn:  # the library kernel on the same shape, for the sustained comparison only
+        from torch.nn.attention import SDPBackend, sdpa_kernel
+        qh = q.transpose(0, 1).unsqueeze(0).contiguous()
+        kx = k.transpose(0, 1).unsqueeze(0).repeat_interleave(4, dim=1).contiguous()
+        vx = v.transpose(0, 1).unsqueeze(0).repeat_interleave(4, dim=1).contiguous()
+
+        def run():
+            with sdpa_kernel([SDPBackend.CUDNN_ATTENTION]):
+                torch.nn.functional.scaled_dot_product_attention(qh, kx, vx, is_causal=True, scale=1 / math.sqrt(128))
     run()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
