@@ -1,7 +1,8 @@
 """Serving-loop soak on the GPU against the live compiled reference
 (development aid; the pytest version is tests/test_serve_fuzz_gpu.py):
 N random ShareGPT-like traces, pools and tier sizes drawn per seed,
-device-virtual execution vs the reference Engine::run.
+device-virtual execution vs the reference Engine::run: requests.csv, the
+CLI's transfer_log.csv / decision_log.csv, and every request's KV bytes.
 
   python scripts/serve_soak.py [--n 24] [--seed0 1000]
 
@@ -55,9 +56,11 @@ def main():
         ids, arr, pr, out = drv.generate_trace(ref, True, n_req, 0, 0, rate, seed)
         t0 = time.perf_counter()
         try:
-            ws, wcsv = drv.run_engine(ref, drv.engine_cfg_struct(model, hw, layerkv=layerkv, gpu_blocks=gpu_blocks,
-                                                                 cpu_blocks=cpu_blocks, seed=seed, tpb=bs,
-                                                                 invariant_checks=True), (ids, arr, pr, out))
+            rcfg = drv.engine_cfg_struct(model, hw, layerkv=layerkv, gpu_blocks=gpu_blocks, cpu_blocks=cpu_blocks,
+                                         seed=seed, tpb=bs, invariant_checks=True)
+            ws, wcsv = drv.run_engine(ref, rcfg, (ids, arr, pr, out))
+            wt = drv.run_engine_log(ref, rcfg, (ids, arr, pr, out), "transfer")
+            wd = drv.run_engine_log(ref, rcfg, (ids, arr, pr, out), "decision")
         except ls.SimulationError as e:  # the reference itself rejects the case: skip it
             print(json.dumps({"seed": seed, "skipped": str(e)}), flush=True)
             continue
@@ -65,12 +68,13 @@ def main():
                                 seed=seed, invariant_checks=True, executor="device-virtual", dense_gemms=False,
                                 prefill_attention=False, verify_kv=True, pinned_frames=pinned,
                                 tokens_per_block=bs, tp_rank=tp_rank)
-        s, rows, csv = serve.run(cfg, serve.Trace(ids, arr, pr, out))
-        ok = csv == wcsv and s["kv_words_mismatched"] == 0 and s["requests_verified"] == len(ids)
+        s, rows, csv, tlog, dlog = serve.run(cfg, serve.Trace(ids, arr, pr, out), logs=True)
+        logs_equal = tlog == wt and dlog == wd
+        ok = csv == wcsv and logs_equal and s["kv_words_mismatched"] == 0 and s["requests_verified"] == len(ids)
         bad += not ok
         print(json.dumps({"seed": seed, "model": kind, "bs": bs, "tp_rank": tp_rank, "requests": n_req, "rate": rate, "gpu_blocks": gpu_blocks, "pinned": pinned,
                           "layerkv": layerkv, "escalations": s["escalations"], "decode_iterations": s["decode_iterations"],
-                          "d2h_jobs": ws["d2h_jobs"], "h2d_jobs": ws["h2d_jobs"], "csv_equal": csv == wcsv,
+                          "d2h_jobs": ws["d2h_jobs"], "h2d_jobs": ws["h2d_jobs"], "csv_equal": csv == wcsv, "cli_logs_equal": logs_equal,
                           "kv_words_mismatched": s["kv_words_mismatched"], "s": round(time.perf_counter() - t0, 1)}),
               flush=True)
     print(json.dumps({"traces": a.n, "mismatched": bad}))
