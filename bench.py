@@ -395,6 +395,7 @@ def prefill_rows(torch, dev_t, link, tf_peak):
     dense()
     attn_ms = min(ev_ms(torch, cs, attn) for _ in range(3))
     flops = 4.0 * d * hq * T * (T + 1) / 2
+    lib = library_attention(torch, cs, q, k, v, out, flops)
     # the same kernel back to back for ~2 s: under the 1000 W cap the clocks
     # settle lower, so this is compared with the sustained cuBLAS figure
     n_sus = 0
@@ -466,6 +467,7 @@ def prefill_rows(torch, dev_t, link, tf_peak):
             "kernel": "prefill_attn2_kernel (tcgen05, causal GQA, two query tiles per CTA)", "shape": f"7B MHA 32 heads, {T} tokens, 1 layer",
             "ms": attn_ms, "tflops": flops / attn_ms / 1e9, "peak_tflops": tf_peak,
             "frac": flops / attn_ms / 1e9 / tf_peak, "flops_counted": "4*d*Hq*T(T+1)/2 (causal QK^T + PV)",
+            "library_cudnn": lib, "ratio_vs_cudnn": (lib["ms"] / attn_ms) if lib.get("ms") else None,
             "sustained": {"launches": n_sus, "ms": sus_ms, "tflops": flops / sus_ms / 1e9,
                           "peak_tflops_sustained": sus_peak, "frac": flops / sus_ms / 1e9 / sus_peak,
                           "clocks": clk_sus.summary(),
@@ -669,7 +671,7 @@ def library_attention(torch, cs, q, k, v, out, flops):
             run()
             ms = min(ev_ms(torch, cs, run) for _ in range(3))
             diff = (res["o"][0].transpose(0, 1).float() - out.float()).abs().max().item()
-        return {"what": "torch SDPA, cuDNN backend only, K/V expanded to Hq heads", "ms": ms,
+        return {"what": "torch SDPA, cuDNN backend only" + (", K/V expanded to Hq heads" if rep > 1 else ""), "ms": ms,
                 "tflops": flops / ms / 1e9, "max_abs_diff_vs_ours": diff}
     except Exception as e:  # noqa: BLE001 - a comparison, never a reason to fail the bench
         return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
